@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the fused D3Q27 cuboid central-moment collide-stream (fp64).
+
+  python bench.py --gpus N --steps K --warmup W [--impl cuda|reference]
+  (N > 1: launched by torchrun, one rank per GPU, NCCL)
+
+Workload (BASELINE.json configs[4], config 5 weak): periodic Taylor-Green vortex,
+512 x 512 x 512 nodes PER GPU (global 512 x 512 x 512N, z-slab decomposition),
+r = 1, s = 2, nu = 0.01, omega_xi = omega_1 = omega_high = 1, FULL_LOCAL
+corrections, fp64.  One step = one pull-stream + collide of every node.
+Metric: MLUPS (10^6 lattice-node updates per second), whole job.
+
+`value` is device-timed (CUDA events on the library's compute stream, max over
+ranks, inputs resident in HBM; the 58 GB per-GPU working set per step is far
+larger than the 126 MB L2, so no flush is needed).  `e2e` is the same metric
+through the public C ABI with HOST buffers: host->device copy of the initial
+fields, K steps, device->host copy of rho and u, all inside the timed region.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "D3Q27 cuboid CM-LBM MLUPS (fp64) at 1/2/4/8 B200; achieved roofline fraction"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
+    ap.add_argument("--workload", default="weak", choices=["weak", "shear", "cavity100", "cavity1000", "tgv"])
+    ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--nz-per-gpu", type=int, default=None, help="override the per-GPU slab depth")
+    return ap.parse_args()
+
+
+def workload(args, world):
+    w = synth.CONFIGS[args.workload]
+    if args.precision == "fp32":
+        w = w.scaled(precision=synth.PREC_FP32)
+    nzl = args.nz_per_gpu or w.nz
+    if args.workload == "weak":
+        w = w.scaled(nz=nzl * world)      # weak scaling: fixed 512^3 per GPU
+    elif w.nz % world:
+        raise SystemExit(f"nz={w.nz} not divisible by {world} GPUs")
+    return w
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi samples of SM clock and throttle reasons DURING the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and
+                          s[3 + i].lower().startswith("active")})
+        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples),
+                "power_w_max": max(pw) if pw else None}
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(workload_name, precision):
+    """dram bytes (read + write) per launch of the collide-stream kernel from the
+    committed ncu --set full summary, if one matches this workload."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as fh:
+        d = json.load(fh)
+    e = d.get(f"{workload_name}/{precision}")
+    return None if e is None else e.get("dram_bytes_per_launch")
+
+
+# --------------------------------------------------------------- cpu oracle
+def oracle_mlups(w, budget_s=15.0, grid=(64, 64, 32), max_steps=None):
+    """The CPU oracle as it stands (single thread), on a bounded sample of the
+    workload: same physics on a smaller grid, as many steps as fit in budget_s."""
+    import oracle as O
+
+    nx, ny, nz = grid
+    ws = w.scaled(nx=nx, ny=ny, nz=nz)
+    o = O.Oracle(**ws.params())
+    rho, u = synth.initial_fields(ws)
+    o.init_fields(rho, u)
+    t0 = time.perf_counter()
+    n = 0
+    while True:
+        o.step(1)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_steps and n >= max_steps):
+            break
+    return ws.nodes * n / el / 1e6, n, ws
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = args.gpus
+    w = workload(args, world)
+    steps, warm = args.steps, args.warmup
+    import oracle as O
+
+    ws = w.scaled(nx=48, ny=48, nz=24)
+    o = O.Oracle(**ws.params())
+    rho, u = synth.initial_fields(ws)
+    o.init_fields(rho, u)
+    for _ in range(warm):
+        o.step(1)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        o.step(1)
+    el = time.perf_counter() - t0
+    v = ws.nodes * steps / el / 1e6
+    sample = f"oracle on {ws.nx}x{ws.ny}x{ws.nz} (same physics as {w.name}), {steps} steps, 1 thread"
+    line = {"metric": METRIC, "value": v, "unit": "MLUPS", "n_gpus": world, "steps": steps, "warmup": warm,
+            "ms_per_step": el / steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": w.name, "nodes_global": w.nodes, "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- cuda arm
+def run_cuda(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2107_14774_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("--gpus N > 1 must be launched with torchrun --nproc-per-node N")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args, world)
+    z0, z1 = synth.slab_range(w.nz, rank, world)
+    kw = w.params()
+    if world > 1:
+        lat = P.distributed_lattice(device=local, **kw)
+    else:
+        lat = P.Lattice(device=local, **kw)
+    stream = lat.stream
+    nloc = w.nx * w.ny * (z1 - z0)
+
+    def init_device():
+        if w.init == "tgv":
+            rho, u = synth.tgv_fields(w.nx, w.ny, w.nz, w.cs2_value, w.u0, z0, z1, w.nz, xp=torch,
+                                      device=torch.device("cuda", local))
+        else:
+            rh, uh = synth.initial_fields(w, z0, z1, w.nz)
+            rho, u = torch.from_numpy(rh).cuda(local), torch.from_numpy(uh).cuda(local)
+        lat.init_fields(rho, u)
+        torch.cuda.synchronize(local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(local)
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    init_device()
+    with torch.cuda.stream(stream):
+        lat.step(args.warmup)
+    barrier()
+
+    # ---- timed region: K steps, one event pair per step on the compute stream
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    l0 = lat.info()["launches"]
+    with ClockSampler(local) as clk:
+        barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            lat.step(1)
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        barrier()
+    launches = lat.info()["launches"] - l0
+    elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end))
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kernel_ms = float(np.mean(step_ms))
+    bad = lat.check(raise_on_unstable=False)["bad_nodes"]
+    mlups = w.nodes * args.steps / (elapsed_ms * 1e-3) / 1e6
+    bpn = lat.info()["bytes_per_node_update"]
+
+    # ---- e2e through the C ABI with host buffers
+    e2e = None
+    if not args.no_e2e:
+        rh = torch.empty((z1 - z0, w.ny, w.nx), dtype=torch.float64, pin_memory=True)
+        uh = torch.empty((3, z1 - z0, w.ny, w.nx), dtype=torch.float64, pin_memory=True)
+        if w.init == "tgv":
+            a, b = synth.tgv_fields(w.nx, w.ny, w.nz, w.cs2_value, w.u0, z0, z1, w.nz, xp=torch,
+                                    device=torch.device("cuda", local))
+            rh.copy_(a)
+            uh.copy_(b)
+            del a, b
+        else:
+            a, b = synth.initial_fields(w, z0, z1, w.nz)
+            rh.copy_(torch.from_numpy(a))
+            uh.copy_(torch.from_numpy(b))
+        ro = torch.empty_like(rh, pin_memory=True)
+        uo = torch.empty_like(uh, pin_memory=True)
+        rn, un, ron, uon = rh.numpy(), uh.numpy(), ro.numpy(), uo.numpy()
+        barrier()
+        t0 = time.perf_counter()
+        lat.init_fields(rn, un)
+        lat.step(args.steps)
+        lat.get_macroscopic(out=(ron, uon))
+        barrier()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        nbytes = 4 * nloc * 8
+        e2e = {"value": w.nodes * args.steps / e2e_s / 1e6, "unit": "MLUPS",
+               "h2d_bytes_per_step": nbytes / args.steps, "d2h_bytes_per_step": nbytes / args.steps,
+               "note": "init_fields(host rho,u) + K steps + get_macroscopic(host), pinned buffers, "
+                       "wall clock with device sync, max over ranks"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = measured_peaks()
+    achieved = bpn * nloc / (kernel_ms * 1e-3) / 1e9
+    prec = "fp64" if w.precision == 0 else "fp32"
+    traffic = ncu_traffic(w.name, prec)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": peak_src,
+            "kernel": "k_collide_stream<double>" if prec == "fp64" else "k_collide_stream<float>",
+            "bytes_per_node": bpn, "nodes_per_launch": nloc if world == 1 else None,
+            "kernel_ms_mean": kernel_ms,
+            "note": "algorithmic bytes 2*27*sizeof(real) per node / mean per-step duration (1 launch per step "
+                    "at N=1; at N>1 the step also holds the boundary-plane launches and the NCCL halo)"}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        v, n, ws = oracle_mlups(w, budget_s=12.0)
+        cpu = {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle",
+               "sample": f"{n} steps of {ws.nx}x{ws.ny}x{ws.nz} (same physics as {w.name}), single thread"}
+    line = {"metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.workload == "weak" else "strong", "vs_baseline": None,
+            "dtype": "f64" if prec == "fp64" else "f64-arith/f32-storage", "data": "synthetic",
+            "config": {"workload": w.name, "grid_global": [w.nx, w.ny, w.nz], "nodes_global": w.nodes,
+                       "r": w.r, "s": w.s, "nu": w.nu, "corrections": "FULL_LOCAL", "storage": prec,
+                       "l2": "working set per step (58 GB/GPU fp64) >> 126 MB L2; no flush needed",
+                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "bad_nodes": bad}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_cuda(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,195 @@
+/*
+ * lbm_cuboid.h -- C ABI of the B200 3D cuboid central-moment LBM (3DCCM-LBM)
+ * hot path (arXiv 2107.14774, Yahia, Schupbach & Premnath).
+ *
+ * "P:Lnnn" cites /root/reference/PAPER.md line nnn.
+ *
+ * The library advances the D3Q27 cuboid-lattice central-moment scheme
+ *   m^c = F S P f;  m~^c = m^c + B^-1 {Lambda (B m^{c,eq} - B m^c) + (I - Lambda/2) B Phi^c};
+ *   f~  = P^-1 S^-1 F^-1 m~^c;  f(x, t+1) = f~(x - e, t)
+ * (Eq. LBEcentralmomentcuboidlattice; step list P:L687-742; collision
+ * App D) with halfway bounce-back and the momentum-augmented
+ * moving wall of Eq. 69, on one GPU or on a z-slab decomposition
+ * over several GPUs (one process per GPU, NCCL halo exchange).
+ *
+ * Conventions
+ *  - Lattice units: dx = dt = 1, dy = r, dz = s.
+ *  - Grid nodes (x, y, z), x fastest.  Host scalar fields are [nz_l][ny][nx],
+ *    host vector fields [3][nz_l][ny][nx], host populations [27][nz_l][ny][nx]
+ *    in the paper's direction order of Eqs. 1a-1c.  nz_l is the
+ *    number of z-planes owned by this rank (nz / world).
+ *  - Canonical state = post-collision populations f~(x, t_n) stored at their
+ *    node (the pull scheme's natural state).  rho and u reported for that
+ *    state are rho = sum f~, u = (sum f~ e - F/2)/rho (the collision adds F to
+ *    the first raw moments).
+ *  - Every function returns 0 (LBM_OK) or a negative lbm_status; the message
+ *    of the last failure on the calling thread is lbm_cuboid_last_error().
+ *  - A handle is thread-compatible, not thread-safe.
+ *  - Host pointers are caller-owned and only read/written during the call.
+ *    Device buffers passed in lbm_cuboid_params are caller-owned (e.g. torch
+ *    tensors) and must outlive the handle.
+ */
+#ifndef LBM_CUBOID_H
+#define LBM_CUBOID_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LBM_CUBOID_ABI_VERSION 1
+
+typedef enum {
+  LBM_OK = 0,
+  LBM_EINVAL = -1,    /* invalid argument / parameter combination */
+  LBM_ENOMEM = -2,    /* device or host allocation failed */
+  LBM_ECUDA = -3,     /* CUDA runtime error (message has the CUDA string) */
+  LBM_ENCCL = -4,     /* NCCL error */
+  LBM_EUNSTABLE = -5, /* NaN, rho <= 0 or |u| > 1 seen by lbm_cuboid_check() */
+  LBM_ENOTSUP = -6    /* built without the requested feature (e.g. NCCL) */
+} lbm_status;
+
+/* Face boundary types.  Faces are ordered -x, +x, -y, +y, -z, +z.  Opposite
+ * faces are both periodic or both non-periodic. */
+typedef enum {
+  LBM_BC_PERIODIC = 0,
+  LBM_BC_BOUNCE_BACK = 1,  /* halfway bounce-back f_q(x_f,t+1) = f~_qbar(x_f,t) (U = 0) */
+  LBM_BC_MOVING_WALL = 2,  /* Eq. 69: +y face only, wall velocity (wall_u, 0, 0) */
+  LBM_BC_FREE_SLIP = 3     /* halfway specular reflection; NOT in the paper (BASELINE config 4) */
+} lbm_bc;
+
+/* Second-order equilibrium corrections (Eqs. 38-40). */
+typedef enum {
+  LBM_CORR_FULL_LOCAL = 0, /* theta with the 3u^2 aliasing terms; local strain rates; lambda = e_rho = 0 */
+  LBM_CORR_LOW_MACH = 1,   /* 3u^2 terms dropped (in theta and in the strain-rate solve) */
+  LBM_CORR_OFF = 2         /* no corrections (ablation) */
+} lbm_corr;
+
+typedef enum {
+  LBM_FP64 = 0,        /* fp64 populations, fp64 arithmetic */
+  LBM_FP32_STORAGE = 1 /* fp32 populations in HBM, fp64 arithmetic in registers */
+} lbm_prec;
+
+typedef enum {
+  LBM_HALO_AUTO = 0, /* 1 GPU + periodic z: wrap inside the kernel; else NCCL ghost planes */
+  LBM_HALO_NCCL = 1  /* always exchange ghost planes with NCCL (also world == 1: send to self) */
+} lbm_halo;
+
+typedef struct {
+  int32_t nx, ny, nz;          /* GLOBAL node counts (>= 1); nz % world == 0 */
+  double r, s;                 /* aspect ratios r = dy/dx, s = dz/dx; > 0 */
+  double cs2;                  /* speed of sound squared; <= 0 -> min(1, r^2, s^2)/3 (DESIGN R3);
+                                  must satisfy 0 < cs2 < min(1, r^2, s^2) */
+  double omega_nu, omega_xi;   /* shear / bulk rates in (0, 2): nu = cs2 (1/omega_nu - 1/2),
+                                  xi = (2 cs2/3)(1/omega_xi - 1/2) (Eq. 53) */
+  double omega_1, omega_high;  /* first-order and all higher-order rates in (0, 2]; paper: 1 */
+  double force[3];             /* constant body force F, lattice units */
+  int32_t bc[6];               /* lbm_bc per face -x,+x,-y,+y,-z,+z */
+  double wall_u;               /* moving-wall speed U along +x (used when bc[3] == LBM_BC_MOVING_WALL) */
+  int32_t corrections;         /* lbm_corr */
+  int32_t precision;           /* lbm_prec */
+  int32_t rank, world;         /* z-slab decomposition: rank owns global planes
+                                  [rank*nz/world, (rank+1)*nz/world) */
+  int32_t device;              /* CUDA device ordinal of this rank */
+  int32_t halo;                /* lbm_halo */
+  const void *nccl_uid;        /* 128-byte ncclUniqueId from lbm_cuboid_nccl_unique_id() on rank 0,
+                                  broadcast by the caller; required iff NCCL ghost exchange is used */
+  void *stream;                /* cudaStream_t for all compute work; NULL -> library-owned stream */
+  void *buf_a, *buf_b;         /* optional caller-owned device buffers of lbm_cuboid_buffer_bytes()
+                                  bytes each (e.g. torch tensors); NULL -> library cudaMalloc */
+} lbm_cuboid_params;
+
+typedef struct lbm_cuboid lbm_cuboid_t;
+
+/* Fill *p with defaults: 32^3, r = s = 1, cs2 auto, omegas 1, periodic, fp64,
+ * rank 0 of 1, device 0, AUTO halo, library-owned stream and buffers. */
+void lbm_cuboid_default_params(lbm_cuboid_params *p);
+
+/* Bytes of ONE population buffer for these parameters:
+ * 27 * nx * ny * (nz/world + 2 ghost planes) * sizeof(real). */
+int lbm_cuboid_buffer_bytes(const lbm_cuboid_params *p, int64_t *bytes);
+
+/* Host-only halo plan of this rank (no GPU needed), element offsets into one
+ * population buffer (layout: DESIGN.md "Data layout"):
+ * out[0] = 1 if ghost planes are exchanged (world > 1 or LBM_HALO_NCCL),
+ * out[1] = peer above (-1 none), out[2] = peer below (-1 none),
+ * out[3] = elements per message (9 * nx * ny),
+ * out[4] = send-up offset (top plane, the 9 directions with e_z = +1),
+ * out[5] = recv-down offset (lower ghost plane, e_z = +1 directions),
+ * out[6] = send-down offset (bottom plane, e_z = -1 directions),
+ * out[7] = recv-up offset (upper ghost plane, e_z = -1 directions).
+ * Every rank issues, inside one NCCL group: send(up), recv(down), send(down),
+ * recv(up), skipping absent peers. */
+int lbm_cuboid_halo_plan(const lbm_cuboid_params *p, int64_t out[8]);
+
+/* Write a fresh 128-byte ncclUniqueId into out (call on rank 0 only). */
+int lbm_cuboid_nccl_unique_id(void *out128);
+
+/* Validate p (errors: LBM_EINVAL with a message naming the field), bind the
+ * device, allocate/bind buffers, upload the parameter block and, if needed,
+ * create the NCCL communicator (collective over all ranks). */
+int lbm_cuboid_create(const lbm_cuboid_params *p, lbm_cuboid_t **out);
+
+/* Initialise the stored state with f~ = f^eq(rho, u + F/(2 rho)) (DESIGN R8)
+ * from HOST fields rho [nz_l][ny][nx] and u [3][nz_l][ny][nx] (fp64).  Fills
+ * the halo ghost planes.  Returns after the device work is enqueued and the
+ * host buffers have been consumed. */
+int lbm_cuboid_init_fields(lbm_cuboid_t *h, const double *rho, const double *u);
+/* Same from DEVICE pointers (fp64, same layouts, on this rank's device). */
+int lbm_cuboid_init_fields_device(lbm_cuboid_t *h, const double *rho, const double *u);
+
+/* Advance nsteps time steps (pull-stream with wall rules, then collide),
+ * asynchronously on the compute stream.  nsteps >= 0. */
+int lbm_cuboid_step(lbm_cuboid_t *h, int64_t nsteps);
+
+/* Block until all enqueued work of the handle is complete; reports
+ * asynchronous CUDA/NCCL failures. */
+int lbm_cuboid_sync(lbm_cuboid_t *h);
+
+/* rho [nz_l][ny][nx] and u [3][nz_l][ny][nx] (fp64) of the stored state into
+ * HOST buffers (synchronises) or into DEVICE buffers (asynchronous). */
+int lbm_cuboid_get_macroscopic(lbm_cuboid_t *h, double *rho, double *u);
+int lbm_cuboid_get_macroscopic_device(lbm_cuboid_t *h, double *rho, double *u);
+
+/* Stored populations, HOST fp64 [27][nz_l][ny][nx], paper direction order.
+ * set_populations also refreshes the halo ghost planes. */
+int lbm_cuboid_get_populations(lbm_cuboid_t *h, double *f);
+/* Planes [z_begin, z_begin + n_planes) of the local slab only: HOST fp64
+ * [27][n_planes][ny][nx], paper direction order. */
+int lbm_cuboid_get_populations_planes(lbm_cuboid_t *h, int32_t z_begin, int32_t n_planes, double *f);
+int lbm_cuboid_set_populations(lbm_cuboid_t *h, const double *f);
+
+/* Rank-local reductions of the stored state, fp64:
+ * out[0] = sum rho, out[1..3] = sum rho u, out[4] = sum rho |u|^2 / 2,
+ * out[5] = max |u|, out[6] = number of nodes with NaN/Inf, rho <= 0 or |u| > 1.
+ * Synchronises.  Returns LBM_EUNSTABLE if out[6] > 0. */
+int lbm_cuboid_check(lbm_cuboid_t *h, double out[7]);
+
+/* Replace the body force (e.g. time-periodic forcing); takes effect for the
+ * steps enqueued after the call. */
+int lbm_cuboid_set_force(lbm_cuboid_t *h, const double force[3]);
+
+/* Introspection:
+ * out[0] = kernel launches enqueued so far by this handle (all kernels),
+ * out[1] = collide-stream launches, out[2] = steps taken,
+ * out[3] = algorithmic bytes per node update (2 * 27 * sizeof(real)),
+ * out[4] = local node count, out[5] = bytes of one buffer,
+ * out[6] = 1 if NCCL ghost exchange is active,
+ * out[7] = 1 if the paper-rate specialisation (omega_1 = omega_high = 1) is used. */
+int lbm_cuboid_info(const lbm_cuboid_t *h, int64_t out[8]);
+
+/* cudaStream_t of the compute stream (for event timing by the caller). */
+void *lbm_cuboid_stream(const lbm_cuboid_t *h);
+
+/* Release library state (streams, events, NCCL comm, library-owned buffers).
+ * Caller-owned buffers are untouched.  NULL is accepted. */
+int lbm_cuboid_destroy(lbm_cuboid_t *h);
+
+/* Message of the last failure on this thread ("" if none). */
+const char *lbm_cuboid_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LBM_CUBOID_H */

@@ -1,0 +1,494 @@
+// cm_kernels.cuh -- sm_100a kernels of the 3D cuboid central-moment LBM
+// (arXiv 2107.14774).  "P:Lnnn" cites /root/reference/PAPER.md line nnn.
+//
+// Layout in HBM: one buffer per time level,
+//   buf[(p*27 + q)*nxy + y*nx + x],  p = z_local + 1 in [0, nz_l + 1]
+// (p = 0 and p = nz_l + 1 are ghost planes filled by the halo exchange), and the
+// internal direction index q = (ex+1) + 3(ey+1) + 9(ez+1) with e in {-1,0,1}^3,
+// so the 9 directions with e_z = -1 / 0 / +1 are contiguous in a plane (one
+// contiguous send/recv region per slab face).
+//
+// The per-node moment transforms are the tensor-product (per-axis) form of
+// m^c = F S P f and f~ = P^-1 S^-1 F^-1 m~^c (Eq. LBEcentralmomentcuboidlattice,
+// P:L676-681): central moments k_mnp = sum_a f_a (e_ax-u_x)^m (e_ay-u_y)^n (e_az-u_z)^p
+// (Eq. 3a) factorise over the three axes, so each of the 27x27
+// transforms is three passes of nine 3-point transforms, all in registers.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace lbm {
+
+constexpr int kBlock = 128;  // threads per block (one node per thread)
+
+// local face treatment (per rank; z faces depend on the slab position)
+enum FaceKind : int {
+  FK_WRAP = 0,        // periodic, wrapped inside the kernel
+  FK_BOUNCE = 1,      // halfway bounce-back (P:L748-749 with U = 0)
+  FK_MOVING = 2,      // Eq. 69 moving wall (+y only)
+  FK_SLIP = 3,        // free-slip (reading R7)
+  FK_GHOST = 4        // neighbour data in a ghost plane (z faces only)
+};
+
+struct Consts {
+  int nx, ny, nzl, nxy;
+  long long plane;      // 27 * nxy elements
+  int face[6];          // FaceKind per local face -x,+x,-y,+y,-z,+z
+  int has_walls;        // any face is BOUNCE/MOVING/SLIP
+  int corr_on;          // corrections != OFF
+  double r, s, cs2;
+  double h1y, h2y, h1z, h2z;  // 1/(2r), 1/(2r^2), 1/(2s), 1/(2s^2)
+  double r2, s2;
+  double wn, wx, w1, wh;      // omega_nu, omega_xi, omega_1, omega_high
+  double an, ab;              // 1/omega_nu - 1/2, 1/omega_xi - 1/2
+  double gx, gy, gz;          // 3cs2 - 1, 3cs2 - r^2, 3cs2 - s^2
+  double galias;              // 1 (FULL_LOCAL: 3u^2 aliasing terms) or 0 (LOW_MACH)
+  double csn, csx;            // 2 cs2/omega_nu, 2 cs2/omega_xi
+  double F[3];
+  double c4, c6;              // cs2^2, cs2^3
+  double lid_u;               // moving-wall speed U
+  double lid_c[3];            // Eq. 69 coefficient per e_z in {-1,0,1}: cs2/(2 r^2) * phi_z(e_z)
+};
+
+// ------------------------------------------------------------------ memory ops
+template <typename T> __device__ __forceinline__ double ldg(const T* p);
+template <> __device__ __forceinline__ double ldg<double>(const double* p) { return __ldg(p); }
+template <> __device__ __forceinline__ double ldg<float>(const float* p) { return (double)__ldg(p); }
+
+template <typename T> __device__ __forceinline__ void stcs(T* p, double v);
+template <> __device__ __forceinline__ void stcs<double>(double* p, double v) { __stcs(p, v); }
+template <> __device__ __forceinline__ void stcs<float>(float* p, double v) { __stcs(p, (float)v); }
+
+#define LBM_Q(i, j, k) ((i) + 3 * (j) + 9 * (k))
+
+// ------------------------------------------------------- per-axis transforms
+// Axis strides in the 3x3x3 slot cube: x -> 1, y -> 3, z -> 9.  A "triple" is
+// the three slots along one axis with the other two indices fixed.
+template <int AX> struct Axis;
+template <> struct Axis<0> { static constexpr int st = 1, o1 = 3, o2 = 9; };
+template <> struct Axis<1> { static constexpr int st = 3, o1 = 1, o2 = 9; };
+template <> struct Axis<2> { static constexpr int st = 9, o1 = 1, o2 = 3; };
+
+// raw moments along one axis, cubic units: (f-, f0, f+) -> (m0, m1, m2)   [App A]
+template <int AX>
+__device__ __forceinline__ void raw_pass(double (&f)[27]) {
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int q = a * Axis<AX>::o1 + b * Axis<AX>::o2;
+      const double fm = f[q], f0 = f[q + Axis<AX>::st], fp = f[q + 2 * Axis<AX>::st];
+      const double sp = fp + fm;
+      f[q] = sp + f0;
+      f[q + Axis<AX>::st] = fp - fm;
+      f[q + 2 * Axis<AX>::st] = sp;
+    }
+}
+
+// scale by the axis speed c (App B, S) and shift to the central frame (App C, F):
+// (m0, m1, m2) -> (m0, c m1 - u m0, c^2 m2 - 2 u c m1 + u^2 m0)
+template <int AX, bool UNIT>
+__device__ __forceinline__ void central_pass(double (&f)[27], double u, double c, double c2) {
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int q = a * Axis<AX>::o1 + b * Axis<AX>::o2;
+      const double m0 = f[q];
+      const double m1 = UNIT ? f[q + Axis<AX>::st] : c * f[q + Axis<AX>::st];
+      const double m2 = UNIT ? f[q + 2 * Axis<AX>::st] : c2 * f[q + 2 * Axis<AX>::st];
+      const double k1 = fma(-u, m0, m1);
+      f[q + Axis<AX>::st] = k1;
+      f[q + 2 * Axis<AX>::st] = fma(-u, m1 + k1, m2);
+    }
+}
+
+// central -> raw (App E, F^-1 = F(-u)), unscale (App F, S^-1) and back to the
+// three populations along the axis (App G, P^-1), with h1 = 1/(2c), h2 = 1/(2c^2):
+// A = k1 + u k0, B = k2 + 2u k1 + u^2 k0;  f0 = k0 - B/c^2, f+- = (B/c^2 +- A/c)/2
+template <int AX>
+__device__ __forceinline__ void inverse_pass(double (&f)[27], double u, double h1, double h2) {
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int q = a * Axis<AX>::o1 + b * Axis<AX>::o2;
+      const double k0 = f[q], k1 = f[q + Axis<AX>::st], k2 = f[q + 2 * Axis<AX>::st];
+      const double A = fma(u, k0, k1);
+      const double B = fma(u, k1 + A, k2);
+      const double t1 = A * h1, t2 = B * h2;
+      f[q] = t2 - t1;
+      f[q + Axis<AX>::st] = fma(-2.0, t2, k0);
+      f[q + 2 * Axis<AX>::st] = t2 + t1;
+    }
+}
+
+// ---------------------------------------------------------------- collision
+// App D on the central moments held in slots K(i,j,k) = f[i+3j+9k].
+// Local strain rates are solved with Cramer's rule on the
+// system divided by rho (one reciprocal); lambda = e_rho = 0 (reading R1).
+__device__ __forceinline__ void second_order_diag(const Consts& c, double rho, double inv_rho,
+                                                  double ux, double uy, double uz,
+                                                  double k200, double k020, double k002,
+                                                  double& o200, double& o020, double& o002) {
+  const double k2s = k200 + k020 + k002;  // B
+  const double k2d1 = k200 - k020;
+  const double k2d2 = k200 - k002;
+  const double c3r = 3.0 * c.cs2 * rho;
+  double e2s = c3r, e2d1 = 0.0, e2d2 = 0.0;
+  if (c.corr_on) {
+    const double ga = 1.5 * c.galias;
+    const double qx = ga * ux * ux, qy = ga * uy * uy, qz = ga * uz * uz;
+    // C coefficients / rho
+    const double Csx = -c.csn + 0.5 * c.gx + qx;
+    const double Cbx = -c.csx + 0.5 * c.gx + qx;
+    const double Csy = c.csn - 0.5 * c.gy - qy;
+    const double Cby = -c.csx + 0.5 * c.gy + qy;
+    const double Csz = c.csn - 0.5 * c.gz - qz;
+    const double Cbz = -c.csx + 0.5 * c.gz + qz;
+    // R / rho with e_rho = 0
+    const double Rb = (k2s - c3r) * inv_rho, Rs1 = k2d1 * inv_rho, Rs2 = k2d2 * inv_rho;
+    const double t1 = Csx * Cbz - Csz * Cbx;
+    const double det = -Csx * Csz * Cby - Csy * t1;
+    const double inv_det = 1.0 / det;
+    const double dxux = (-Csz * Cby * Rs1 - Csy * (Cbz * Rs2 - Csz * Rb)) * inv_det;
+    const double dyuy = (Csx * (Rs2 * Cbz - Csz * Rb) - Rs1 * t1) * inv_det;
+    const double dzuz = (Csx * Cby * (Rs1 - Rs2) - Csy * (Csx * Rb - Rs2 * Cbx)) * inv_det;
+    // theta / (-rho (1/omega - 1/2)) times the strain rates
+    const double tx = (2.0 * qx + c.gx) * dxux;
+    const double ty = (2.0 * qy + c.gy) * dyuy;
+    const double tz = (2.0 * qz + c.gz) * dzuz;
+    const double rn = rho * c.an, rb = rho * c.ab;
+    e2d1 = -rn * (tx - ty);          // Eq. 63
+    e2d2 = -rn * (tx - tz);          // Eq. 63
+    e2s = c3r - rb * (tx + ty + tz); // Eq. 63
+  }
+  const double s2s = fma(c.wx, e2s - k2s, k2s);
+  const double s2d1 = fma(c.wn, e2d1 - k2d1, k2d1);
+  const double s2d2 = fma(c.wn, e2d2 - k2d2, k2d2);
+  const double third = 1.0 / 3.0;  // B^-1
+  o200 = (s2s + s2d1 + s2d2) * third;
+  o020 = (s2s - 2.0 * s2d1 + s2d2) * third;
+  o002 = (s2s + s2d1 - 2.0 * s2d2) * third;
+}
+
+// Generic relaxation (any omega_1, omega_high): all 27 central moments are in f.
+__device__ __forceinline__ void collide_generic(const Consts& c, double (&f)[27], double rho,
+                                                double inv_rho, double ux, double uy, double uz) {
+#define K(i, j, k) f[LBM_Q(i, j, k)]
+  const double w1 = c.w1, wn = c.wn, wh = c.wh;
+  // first order: k~ = k + w1 (0 - k) + (1 - w1/2) F
+  K(1, 0, 0) = fma(1.0 - w1, K(1, 0, 0), (1.0 - 0.5 * w1) * c.F[0]);
+  K(0, 1, 0) = fma(1.0 - w1, K(0, 1, 0), (1.0 - 0.5 * w1) * c.F[1]);
+  K(0, 0, 1) = fma(1.0 - w1, K(0, 0, 1), (1.0 - 0.5 * w1) * c.F[2]);
+  // off-diagonal second order
+  K(1, 1, 0) *= (1.0 - wn);
+  K(1, 0, 1) *= (1.0 - wn);
+  K(0, 1, 1) *= (1.0 - wn);
+  double o200, o020, o002;
+  second_order_diag(c, rho, inv_rho, ux, uy, uz, K(2, 0, 0), K(0, 2, 0), K(0, 0, 2), o200, o020, o002);
+  K(2, 0, 0) = o200;
+  K(0, 2, 0) = o020;
+  K(0, 0, 2) = o002;
+  // third and higher orders: every B group has one rate, so B^-1 Lambda B acts
+  // as omega_high on each moment; equilibria of Eq. 64
+  const double om = 1.0 - wh;
+  K(1, 2, 0) *= om; K(1, 0, 2) *= om; K(2, 1, 0) *= om;
+  K(0, 1, 2) *= om; K(2, 0, 1) *= om; K(0, 2, 1) *= om;
+  K(1, 1, 1) *= om;
+  K(2, 1, 1) *= om; K(1, 2, 1) *= om; K(1, 1, 2) *= om;
+  K(1, 2, 2) *= om; K(2, 1, 2) *= om; K(2, 2, 1) *= om;
+  const double e4 = wh * c.c4 * rho;
+  K(2, 2, 0) = fma(om, K(2, 2, 0), e4);
+  K(2, 0, 2) = fma(om, K(2, 0, 2), e4);
+  K(0, 2, 2) = fma(om, K(0, 2, 2), e4);
+  K(2, 2, 2) = fma(om, K(2, 2, 2), wh * c.c6 * rho);
+#undef K
+}
+
+// -------------------------------------------------------------- streaming
+// Gather the 27 incoming populations of node (x, y, z) (pull form).
+// Fast path: no wall face adjacent -> periodic/ghost addressing only.
+template <typename T>
+__device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& c, int x, int y, int z,
+                                       double (&f)[27]) {
+  const int nx = c.nx;
+  const int xm = (x == 0) ? nx - 1 : x - 1;        // source of e_x = +1
+  const int xp = (x == nx - 1) ? 0 : x + 1;        // source of e_x = -1
+  const int ym = (y == 0) ? c.ny - 1 : y - 1;
+  const int yp = (y == c.ny - 1) ? 0 : y + 1;
+  int zm = z - 1, zp = z + 1;                      // -1 / nz_l address ghost planes
+  if (z == 0 && c.face[4] == FK_WRAP) zm = c.nzl - 1;
+  if (z == c.nzl - 1 && c.face[5] == FK_WRAP) zp = 0;
+  const int sx[3] = {xp, x, xm};                   // index by e + 1
+  const int sy[3] = {yp * nx, y * nx, ym * nx};
+  const T* pz[3] = {src + (long long)(zp + 1) * c.plane, src + (long long)(z + 1) * c.plane,
+                    src + (long long)(zm + 1) * c.plane};
+
+  bool wall = false;
+  if (c.has_walls) {
+    wall = (x == 0 && c.face[0] >= FK_BOUNCE && c.face[0] <= FK_SLIP) ||
+           (x == nx - 1 && c.face[1] >= FK_BOUNCE && c.face[1] <= FK_SLIP) ||
+           (y == 0 && c.face[2] >= FK_BOUNCE && c.face[2] <= FK_SLIP) ||
+           (y == c.ny - 1 && c.face[3] >= FK_BOUNCE && c.face[3] <= FK_SLIP) ||
+           (z == 0 && c.face[4] >= FK_BOUNCE && c.face[4] <= FK_SLIP) ||
+           (z == c.nzl - 1 && c.face[5] >= FK_BOUNCE && c.face[5] <= FK_SLIP);
+  }
+  if (!wall) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int q = LBM_Q(i, j, k);
+          f[q] = ldg(pz[k] + q * c.nxy + sy[j] + sx[i]);
+        }
+    return;
+  }
+  // Wall-adjacent node.  Crossing kind of the source of displacement e per axis:
+  // 0 none (inside, periodic or ghost), 1 no-slip, 2 moving wall, 3 free-slip.
+  auto kind = [](int fk) { return (fk >= FK_BOUNCE && fk <= FK_SLIP) ? fk : 0; };
+  const int cxp = (x == 0) ? kind(c.face[0]) : 0, cxm = (x == nx - 1) ? kind(c.face[1]) : 0;
+  const int cyp = (y == 0) ? kind(c.face[2]) : 0, cym = (y == c.ny - 1) ? kind(c.face[3]) : 0;
+  const int czp = (z == 0) ? kind(c.face[4]) : 0, czm = (z == c.nzl - 1) ? kind(c.face[5]) : 0;
+  const int own = y * nx + x;
+  const T* p0 = pz[1];
+  double rho_f = 0.0;  // reading R4: rho_f = sum_b f~_b(x_f, t) at the wall-adjacent node
+  if (cym == FK_MOVING) {
+#pragma unroll
+    for (int q = 0; q < 27; ++q) rho_f += ldg(p0 + q * c.nxy + own);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int q = LBM_Q(i, j, k);
+        const int ex = i - 1, ey = j - 1, ez = k - 1;
+        const int kx = ex > 0 ? cxp : (ex < 0 ? cxm : 0);
+        const int ky = ey > 0 ? cyp : (ey < 0 ? cym : 0);
+        const int kz = ez > 0 ? czp : (ez < 0 ? czm : 0);
+        const bool noslip = (kx == FK_BOUNCE || kx == FK_MOVING) || (ky == FK_BOUNCE || ky == FK_MOVING) ||
+                            (kz == FK_BOUNCE || kz == FK_MOVING);
+        if (noslip) {
+          // halfway bounce-back from the own node's opposite direction
+          double v = ldg(p0 + LBM_Q(2 - i, 2 - j, 2 - k) * c.nxy + own);
+          if (ky == FK_MOVING)  // Eq. 69: + rho_f U e_x cs2/(2 r^2) phi_z(e_z)
+            v = fma(rho_f * c.lid_u * (double)ex, c.lid_c[k], v);
+          f[q] = v;
+        } else {
+          // free-slip (reading R7): mirror the crossed axes, source at the own
+          // coordinate along them; otherwise the periodic/ghost neighbour
+          const bool mx = (kx == FK_SLIP), my = (ky == FK_SLIP), mz = (kz == FK_SLIP);
+          const int qi = mx ? 2 - i : i, qj = my ? 2 - j : j, qk = mz ? 2 - k : k;
+          const int xs = mx ? x : sx[i];
+          const int ys = my ? y * nx : sy[j];
+          const T* zs = mz ? p0 : pz[k];
+          f[q] = ldg(zs + LBM_Q(qi, qj, qk) * c.nxy + ys + xs);
+        }
+      }
+}
+
+// --------------------------------------------------------- the fused kernel
+// One thread per node of planes [zbeg, zbeg + gridDim.y) of the local slab.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_collide_stream(const T* __restrict__ src, T* __restrict__ dst,
+                                                           const __grid_constant__ Consts c, int zbeg) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int y = idx / c.nx;
+  const int x = idx - y * c.nx;
+  const int z = zbeg + blockIdx.y;
+
+  double f[27];
+  gather<T>(src, c, x, y, z, f);
+
+  // m = P f (App A), per axis
+  raw_pass<0>(f);
+  raw_pass<1>(f);
+  raw_pass<2>(f);
+  // rho, u (Eq. 12); y/z first moments carry the S factors r, s
+  const double rho = f[LBM_Q(0, 0, 0)];
+  const double inv_rho = 1.0 / rho;
+  const double ux = (f[LBM_Q(1, 0, 0)] + 0.5 * c.F[0]) * inv_rho;
+  const double uy = fma(c.r, f[LBM_Q(0, 1, 0)], 0.5 * c.F[1]) * inv_rho;
+  const double uz = fma(c.s, f[LBM_Q(0, 0, 1)], 0.5 * c.F[2]) * inv_rho;
+  // m^c = F S m (App B + App C), per axis
+  central_pass<0, true>(f, ux, 1.0, 1.0);
+  central_pass<1, false>(f, uy, c.r, c.r2);
+  central_pass<2, false>(f, uz, c.s, c.s2);
+
+  collide_generic(c, f, rho, inv_rho, ux, uy, uz);
+
+  // f~ = P^-1 S^-1 F^-1 m~^c (App E, F, G), per axis
+  inverse_pass<2>(f, uz, c.h1z, c.h2z);
+  inverse_pass<1>(f, uy, c.h1y, c.h2y);
+  inverse_pass<0>(f, ux, 0.5, 0.5);
+
+  T* out = dst + (long long)(z + 1) * c.plane + idx;
+#pragma unroll
+  for (int q = 0; q < 27; ++q) stcs<T>(out + q * c.nxy, f[q]);
+}
+
+// -------------------------------------------------------------- init kernel
+// f~ = f^eq(rho, u + F/(2 rho)) (reading R8).  The raw equilibria of Eq. 10
+// factorise per axis into 1D Maxwellian moments (1, u, cs2 + u^2), so
+// f^eq_a = rho phi_x(e_x) phi_y(e_y) phi_z(e_z) with
+// phi(0) = 1 - (cs2 + u^2)/c^2, phi(+-1) = ((cs2 + u^2)/c^2 +- u/c)/2.
+__device__ __forceinline__ void axis_phi(double u, double c, double cs2, double (&p)[3]) {
+  const double a = (cs2 + u * u) / (c * c);
+  const double b = u / c;
+  p[0] = 0.5 * (a - b);
+  p[1] = 1.0 - a;
+  p[2] = 0.5 * (a + b);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_init(const double* __restrict__ rho_in, const double* __restrict__ u_in,
+                                                 long long ustride, T* __restrict__ dst,
+                                                 const __grid_constant__ Consts c, int zbeg) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const long long n = (long long)blockIdx.y * c.nxy + idx;
+  const double rho = rho_in[n];
+  const double ux = u_in[n] + 0.5 * c.F[0] / rho;
+  const double uy = u_in[n + ustride] + 0.5 * c.F[1] / rho;
+  const double uz = u_in[n + 2 * ustride] + 0.5 * c.F[2] / rho;
+  double px[3], py[3], pz[3];
+  axis_phi(ux, 1.0, c.cs2, px);
+  axis_phi(uy, c.r, c.cs2, py);
+  axis_phi(uz, c.s, c.cs2, pz);
+  T* out = dst + (long long)(zbeg + blockIdx.y + 1) * c.plane + idx;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) stcs<T>(out + LBM_Q(i, j, k) * c.nxy, rho * px[i] * py[j] * pz[k]);
+}
+
+// -------------------------------------------------------- macroscopic kernel
+// rho = sum f~, u = (sum f~ e - F/2)/rho of the stored post-collision state.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_macro(const T* __restrict__ src, double* __restrict__ rho_out,
+                                                  double* __restrict__ u_out, long long ustride,
+                                                  const __grid_constant__ Consts c, int zbeg) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const T* p = src + (long long)(zbeg + blockIdx.y + 1) * c.plane + idx;
+  double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const double v = ldg(p + LBM_Q(i, j, k) * c.nxy);
+        rho += v;
+        jx += (double)(i - 1) * v;
+        jy += (double)(j - 1) * v;
+        jz += (double)(k - 1) * v;
+      }
+  const long long n = (long long)blockIdx.y * c.nxy + idx;
+  const double inv = 1.0 / rho;
+  rho_out[n] = rho;
+  u_out[n] = (jx - 0.5 * c.F[0]) * inv;
+  u_out[n + ustride] = (c.r * jy - 0.5 * c.F[1]) * inv;
+  u_out[n + 2 * ustride] = (c.s * jz - 0.5 * c.F[2]) * inv;
+}
+
+// ---------------------------------------------------------- pack / unpack
+// Paper direction order (Eqs. 1a-1c) <-> internal order; staging layout
+// [27][nplanes][nxy] in the paper order.
+__constant__ int8_t kPaperToInternal[27] = {
+    // paper a: (ex,ey,ez) -> (ex+1) + 3(ey+1) + 9(ez+1)
+    13, 14, 12, 16, 10, 22, 4, 17, 15, 11, 9, 23, 21, 5, 3, 25, 19, 7, 1, 26, 24, 20, 18, 8, 6, 2, 0};
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_pack(const T* __restrict__ src, double* __restrict__ stage, int nplanes,
+                                                 const __grid_constant__ Consts c, int zbeg) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int zz = blockIdx.y;
+  const T* p = src + (long long)(zbeg + zz + 1) * c.plane + idx;
+  for (int a = 0; a < 27; ++a)
+    stage[((long long)a * nplanes + zz) * c.nxy + idx] = ldg(p + kPaperToInternal[a] * c.nxy);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_unpack(const double* __restrict__ stage, T* __restrict__ dst, int nplanes,
+                                                   const __grid_constant__ Consts c, int zbeg) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int zz = blockIdx.y;
+  T* p = dst + (long long)(zbeg + zz + 1) * c.plane + idx;
+  for (int a = 0; a < 27; ++a) p[kPaperToInternal[a] * c.nxy] = (T)stage[((long long)a * nplanes + zz) * c.nxy + idx];
+}
+
+// -------------------------------------------------------------- check kernel
+// out[0] sum rho, out[1..3] sum rho u, out[4] sum rho|u|^2/2, out[5] max|u| (as
+// ordered bits of a non-negative double), out[6] count of bad nodes.
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_check(const T* __restrict__ src, double* __restrict__ out,
+                                                  const __grid_constant__ Consts c) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  const int z = blockIdx.y;
+  double v[7] = {0, 0, 0, 0, 0, 0, 0};
+  if (idx < c.nxy) {
+    const T* p = src + (long long)(z + 1) * c.plane + idx;
+    double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
+    for (int q = 0; q < 27; ++q) {
+      const double fv = ldg(p + q * c.nxy);
+      const int i = q % 3, j = (q / 3) % 3, k = q / 9;
+      rho += fv;
+      jx += (i - 1) * fv;
+      jy += (j - 1) * fv;
+      jz += (k - 1) * fv;
+    }
+    const double ux = (jx - 0.5 * c.F[0]) / rho, uy = (c.r * jy - 0.5 * c.F[1]) / rho,
+                 uz = (c.s * jz - 0.5 * c.F[2]) / rho;
+    const double u2 = ux * ux + uy * uy + uz * uz;
+    v[0] = rho;
+    v[1] = rho * ux;
+    v[2] = rho * uy;
+    v[3] = rho * uz;
+    v[4] = 0.5 * rho * u2;
+    v[5] = sqrt(u2);
+    const bool bad = !(rho > 0.0) || !(u2 <= 1.0) || !isfinite(rho) || !isfinite(u2);
+    v[6] = bad ? 1.0 : 0.0;
+    if (bad) v[5] = 0.0;
+  }
+  __shared__ double sm[7][kBlock / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < 7; ++t) {
+    const double r = (t == 5) ? warp_max(v[t]) : warp_sum(v[t]);
+    if (lane == 0) sm[t][w] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    const int t = threadIdx.x;
+    double r = sm[t][0];
+    for (int i = 1; i < kBlock / 32; ++i) r = (t == 5) ? fmax(r, sm[t][i]) : r + sm[t][i];
+    if (t == 5)
+      atomicMax(reinterpret_cast<unsigned long long*>(out + 5), (unsigned long long)__double_as_longlong(r));
+    else
+      atomicAdd(out + t, r);
+  }
+}
+
+}  // namespace lbm

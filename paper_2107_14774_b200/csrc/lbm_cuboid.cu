@@ -1,0 +1,641 @@
+// lbm_cuboid.cu -- runtime and C ABI (include/lbm_cuboid.h) of the B200
+// 3D cuboid central-moment LBM.  One handle = one z-slab on one GPU.
+//
+// Per time step:
+//   single GPU, periodic or walled z : one fused collide-stream launch over all
+//                                      planes (z wrap inside the kernel)
+//   ghost-plane mode (world > 1, or LBM_HALO_NCCL):
+//     compute stream: wait(halo[t-1]) -> boundary planes {0, nz_l-1} -> record(bnd)
+//     comm stream   : wait(bnd) -> NCCL send/recv of the 9 outgoing directions of
+//                     the two boundary planes into the neighbours' ghost planes
+//                     -> record(halo[t])
+//     compute stream: interior planes 1..nz_l-2 (overlaps the exchange)
+#include "../../include/lbm_cuboid.h"
+#include "cm_kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using lbm::Consts;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CU(call)                                                                                     \
+  do {                                                                                               \
+    cudaError_t e_ = (call);                                                                         \
+    if (e_ != cudaSuccess) return fail(LBM_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,         \
+                                       cudaGetErrorString(e_));                                      \
+  } while (0)
+
+#define NC(call)                                                                                     \
+  do {                                                                                               \
+    ncclResult_t r_ = (call);                                                                        \
+    if (r_ != ncclSuccess) return fail(LBM_ENCCL, "%s:%d %s: %s", __FILE__, __LINE__, #call,         \
+                                       ncclGetErrorString(r_));                                      \
+  } while (0)
+
+constexpr size_t kStageBytes = size_t(256) << 20;  // host<->device staging chunk
+
+}  // namespace
+
+struct lbm_cuboid {
+  lbm_cuboid_params p{};
+  int nzl = 0, z0 = 0;
+  int64_t nxy = 0, plane = 0, buf_elems = 0;
+  size_t elem = 8;
+  void* buf[2] = {nullptr, nullptr};
+  bool own_buf = false;
+  int cur = 0;  // buf[cur] holds the stored state
+  cudaStream_t stream = nullptr, comm_stream = nullptr;
+  bool own_stream = false;
+  cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
+  bool halo_pending = false;
+  bool ghost = false;  // ghost-plane (NCCL) mode
+  ncclComm_t comm = nullptr;
+  int peer_down = -1, peer_up = -1;  // ranks owning the planes below / above, -1 none
+  Consts c{};
+  double* stage = nullptr;
+  size_t stage_bytes = 0;
+  double* d_check = nullptr;
+  int64_t launches = 0, cs_launches = 0, steps = 0;
+};
+
+namespace {
+
+int set_device(const lbm_cuboid* h) {
+  CU(cudaSetDevice(h->p.device));
+  return LBM_OK;
+}
+
+int validate(const lbm_cuboid_params* p) {
+  if (!p) return fail(LBM_EINVAL, "params is NULL");
+  if (p->nx < 1 || p->ny < 1 || p->nz < 1) return fail(LBM_EINVAL, "nx, ny, nz must be >= 1");
+  if (p->world < 1 || p->rank < 0 || p->rank >= p->world) return fail(LBM_EINVAL, "rank/world out of range");
+  if (p->nz % p->world) return fail(LBM_EINVAL, "nz (%d) must be divisible by world (%d)", p->nz, p->world);
+  if (!(p->r > 0) || !(p->s > 0) || !std::isfinite(p->r) || !std::isfinite(p->s))
+    return fail(LBM_EINVAL, "aspect ratios r, s must be finite and > 0");
+  const double lim = std::min({1.0, p->r * p->r, p->s * p->s});
+  const double cs2 = p->cs2 > 0 ? p->cs2 : lim / 3.0;
+  if (!(cs2 > 0 && cs2 < lim)) return fail(LBM_EINVAL, "cs2 = %g must satisfy 0 < cs2 < min(1, r^2, s^2) = %g", cs2, lim);
+  auto bad_w = [](double w) { return !(w > 0.0 && w < 2.0); };
+  if (bad_w(p->omega_nu) || bad_w(p->omega_xi)) return fail(LBM_EINVAL, "omega_nu, omega_xi must lie in (0, 2)");
+  if (!(p->omega_1 > 0 && p->omega_1 <= 2) || !(p->omega_high > 0 && p->omega_high <= 2))
+    return fail(LBM_EINVAL, "omega_1, omega_high must lie in (0, 2]");
+  for (int f = 0; f < 6; ++f)
+    if (p->bc[f] < 0 || p->bc[f] > 3) return fail(LBM_EINVAL, "bc[%d] = %d is not an lbm_bc", f, p->bc[f]);
+  for (int d = 0; d < 3; ++d)
+    if ((p->bc[2 * d] == LBM_BC_PERIODIC) != (p->bc[2 * d + 1] == LBM_BC_PERIODIC))
+      return fail(LBM_EINVAL, "faces %d and %d must be both periodic or both non-periodic", 2 * d, 2 * d + 1);
+  for (int f = 0; f < 6; ++f)
+    if (p->bc[f] == LBM_BC_MOVING_WALL && f != 3)
+      return fail(LBM_EINVAL, "configuration error: a moving wall is supported on the +y face only (P:L751)");
+  if (p->corrections < 0 || p->corrections > 2) return fail(LBM_EINVAL, "corrections must be an lbm_corr");
+  if (p->precision < 0 || p->precision > 1) return fail(LBM_EINVAL, "precision must be an lbm_prec");
+  if (p->halo < 0 || p->halo > 1) return fail(LBM_EINVAL, "halo must be an lbm_halo");
+  for (int d = 0; d < 3; ++d)
+    if (!std::isfinite(p->force[d])) return fail(LBM_EINVAL, "force must be finite");
+  if (!std::isfinite(p->wall_u)) return fail(LBM_EINVAL, "wall_u must be finite");
+  const int64_t nxy = int64_t(p->nx) * p->ny;
+  if (27 * nxy >= (int64_t(1) << 31)) return fail(LBM_EINVAL, "nx*ny too large (27*nx*ny must fit int32)");
+  if (p->nz / p->world > 65535) return fail(LBM_EINVAL, "nz/world must be <= 65535");
+  return LBM_OK;
+}
+
+void fill_consts(lbm_cuboid* h) {
+  const lbm_cuboid_params& p = h->p;
+  Consts& c = h->c;
+  c.nx = p.nx;
+  c.ny = p.ny;
+  c.nzl = h->nzl;
+  c.nxy = int(h->nxy);
+  c.plane = h->plane;
+  const double cs2 = p.cs2 > 0 ? p.cs2 : std::min({1.0, p.r * p.r, p.s * p.s}) / 3.0;
+  c.r = p.r;
+  c.s = p.s;
+  c.cs2 = cs2;
+  c.r2 = p.r * p.r;
+  c.s2 = p.s * p.s;
+  c.h1y = 0.5 / p.r;
+  c.h2y = 0.5 / (p.r * p.r);
+  c.h1z = 0.5 / p.s;
+  c.h2z = 0.5 / (p.s * p.s);
+  c.wn = p.omega_nu;
+  c.wx = p.omega_xi;
+  c.w1 = p.omega_1;
+  c.wh = p.omega_high;
+  c.an = 1.0 / p.omega_nu - 0.5;
+  c.ab = 1.0 / p.omega_xi - 0.5;
+  c.gx = 3.0 * cs2 - 1.0;
+  c.gy = 3.0 * cs2 - c.r2;
+  c.gz = 3.0 * cs2 - c.s2;
+  c.galias = (p.corrections == LBM_CORR_FULL_LOCAL) ? 1.0 : 0.0;
+  c.corr_on = (p.corrections != LBM_CORR_OFF);
+  c.csn = 2.0 * cs2 / p.omega_nu;
+  c.csx = 2.0 * cs2 / p.omega_xi;
+  for (int d = 0; d < 3; ++d) c.F[d] = p.force[d];
+  c.c4 = cs2 * cs2;
+  c.c6 = cs2 * cs2 * cs2;
+  c.lid_u = (p.bc[3] == LBM_BC_MOVING_WALL) ? p.wall_u : 0.0;
+  // Eq. 69 coefficients: f^eq_a - f^eq_abar at the wall (u = (U,0,0)) is
+  // rho U e_x * cs2/(2 r^2) * phi_z(e_z), phi_z(0) = 1 - cs2/s^2, phi_z(+-1) = cs2/(2 s^2)
+  const double py = cs2 / (2.0 * c.r2);
+  c.lid_c[0] = py * cs2 / (2.0 * c.s2);
+  c.lid_c[1] = py * (1.0 - cs2 / c.s2);
+  c.lid_c[2] = py * cs2 / (2.0 * c.s2);
+  // local faces
+  auto kind = [](int bc) {
+    switch (bc) {
+      case LBM_BC_BOUNCE_BACK: return int(lbm::FK_BOUNCE);
+      case LBM_BC_MOVING_WALL: return int(lbm::FK_MOVING);
+      case LBM_BC_FREE_SLIP: return int(lbm::FK_SLIP);
+      default: return int(lbm::FK_WRAP);
+    }
+  };
+  for (int f = 0; f < 4; ++f) c.face[f] = kind(p.bc[f]);
+  const bool zper = (p.bc[4] == LBM_BC_PERIODIC);
+  if (h->ghost) {
+    c.face[4] = (p.rank == 0 && !zper) ? kind(p.bc[4]) : int(lbm::FK_GHOST);
+    c.face[5] = (p.rank == p.world - 1 && !zper) ? kind(p.bc[5]) : int(lbm::FK_GHOST);
+  } else {
+    c.face[4] = kind(p.bc[4]);
+    c.face[5] = kind(p.bc[5]);
+  }
+  c.has_walls = 0;
+  for (int f = 0; f < 6; ++f)
+    if (c.face[f] >= lbm::FK_BOUNCE && c.face[f] <= lbm::FK_SLIP) c.has_walls = 1;
+}
+
+dim3 grid_for(const lbm_cuboid* h, int nplanes) {
+  return dim3(unsigned((h->nxy + lbm::kBlock - 1) / lbm::kBlock), unsigned(nplanes), 1);
+}
+
+int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, cudaStream_t s) {
+  if (nplanes <= 0) return LBM_OK;
+  dim3 g = grid_for(h, nplanes);
+  if (h->p.precision == LBM_FP64)
+    lbm::k_collide_stream<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg);
+  else
+    lbm::k_collide_stream<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg);
+  CU(cudaGetLastError());
+  h->launches++;
+  h->cs_launches++;
+  return LBM_OK;
+}
+
+// Halo plan (element offsets into one buffer): see lbm_cuboid_halo_plan().
+struct HaloPlan {
+  bool ghost;
+  int peer_up, peer_down;
+  int64_t count, send_up, recv_dn, send_dn, recv_up;
+};
+
+HaloPlan make_plan(const lbm_cuboid_params* p) {
+  HaloPlan hp{};
+  const bool zper = (p->bc[4] == LBM_BC_PERIODIC);
+  hp.ghost = (p->world > 1) || (p->halo == LBM_HALO_NCCL && zper);
+  hp.peer_up = hp.peer_down = -1;
+  if (hp.ghost) {
+    hp.peer_up = (p->rank < p->world - 1 || zper) ? (p->rank + 1) % p->world : -1;
+    hp.peer_down = (p->rank > 0 || zper) ? (p->rank - 1 + p->world) % p->world : -1;
+  }
+  const int64_t nxy = int64_t(p->nx) * p->ny, plane = 27 * nxy, nzl = p->nz / p->world;
+  hp.count = 9 * nxy;
+  // internal q = (ex+1) + 3(ey+1) + 9(ez+1): q 0..8 have e_z = -1, q 18..26 e_z = +1
+  hp.send_up = nzl * plane + 18 * nxy;        // plane p = nz_l (z = nz_l - 1)
+  hp.recv_dn = 0 * plane + 18 * nxy;          // ghost p = 0, pulled by z = 0
+  hp.send_dn = 1 * plane + 0 * nxy;           // plane p = 1 (z = 0)
+  hp.recv_up = (nzl + 1) * plane + 0 * nxy;   // ghost p = nz_l + 1, pulled by z = nz_l - 1
+  return hp;
+}
+
+// NCCL exchange of buffer `which`'s boundary planes into the neighbours' ghost
+// planes, on the comm stream, after the work already enqueued on the compute stream.
+int exchange(lbm_cuboid* h, int which) {
+  if (!h->ghost) return LBM_OK;
+  CU(cudaEventRecord(h->ev_bnd, h->stream));
+  CU(cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
+  const HaloPlan hp = make_plan(&h->p);
+  const ncclDataType_t dt = (h->p.precision == LBM_FP64) ? ncclDouble : ncclFloat;
+  char* b = (char*)h->buf[which];
+  const size_t e = h->elem, cnt = size_t(hp.count);
+  // NCCL matches the sends and recvs between one pair of ranks in issue order;
+  // this order is right also when both neighbours are one rank (world 2,
+  // periodic) or this rank itself (world 1): the k-th send meets the k-th recv.
+  NC(ncclGroupStart());
+  if (hp.peer_up >= 0) NC(ncclSend(b + hp.send_up * e, cnt, dt, hp.peer_up, h->comm, h->comm_stream));
+  if (hp.peer_down >= 0) NC(ncclRecv(b + hp.recv_dn * e, cnt, dt, hp.peer_down, h->comm, h->comm_stream));
+  if (hp.peer_down >= 0) NC(ncclSend(b + hp.send_dn * e, cnt, dt, hp.peer_down, h->comm, h->comm_stream));
+  if (hp.peer_up >= 0) NC(ncclRecv(b + hp.recv_up * e, cnt, dt, hp.peer_up, h->comm, h->comm_stream));
+  NC(ncclGroupEnd());
+  CU(cudaEventRecord(h->ev_halo, h->comm_stream));
+  h->halo_pending = true;
+  return LBM_OK;
+}
+
+int wait_halo(lbm_cuboid* h) {
+  if (h->halo_pending) {
+    CU(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
+    h->halo_pending = false;
+  }
+  return LBM_OK;
+}
+
+int ensure_stage(lbm_cuboid* h, size_t bytes) {
+  if (h->stage_bytes >= bytes) return LBM_OK;
+  if (h->stage) {
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaFree(h->stage));
+    h->stage = nullptr;
+    h->stage_bytes = 0;
+  }
+  if (cudaMalloc(&h->stage, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(LBM_ENOMEM, "cudaMalloc(%zu) for the staging buffer failed", bytes);
+  }
+  h->stage_bytes = bytes;
+  return LBM_OK;
+}
+
+// planes per staging chunk for `per_node` doubles per node
+int chunk_planes(const lbm_cuboid* h, int per_node) {
+  const size_t per_plane = size_t(per_node) * size_t(h->nxy) * sizeof(double);
+  return int(std::max<size_t>(1, std::min<size_t>(h->nzl, kStageBytes / per_plane)));
+}
+
+template <typename T>
+int init_kernel(lbm_cuboid* h, const double* rho, const double* u, long long ustride, int zbeg, int n) {
+  lbm::k_init<T><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>(rho, u, ustride, (T*)h->buf[h->cur], h->c, zbeg);
+  CU(cudaGetLastError());
+  h->launches++;
+  return LBM_OK;
+}
+
+int run_init(lbm_cuboid* h, const double* rho, const double* u, long long ustride, int zbeg, int n) {
+  return (h->p.precision == LBM_FP64) ? init_kernel<double>(h, rho, u, ustride, zbeg, n)
+                                       : init_kernel<float>(h, rho, u, ustride, zbeg, n);
+}
+
+int run_macro(lbm_cuboid* h, double* rho, double* u, long long ustride, int zbeg, int n) {
+  if (h->p.precision == LBM_FP64)
+    lbm::k_macro<double><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], rho, u,
+                                                                        ustride, h->c, zbeg);
+  else
+    lbm::k_macro<float><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], rho, u,
+                                                                       ustride, h->c, zbeg);
+  CU(cudaGetLastError());
+  h->launches++;
+  return LBM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void lbm_cuboid_default_params(lbm_cuboid_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->nx = p->ny = p->nz = 32;
+  p->r = p->s = 1.0;
+  p->cs2 = 0.0;
+  p->omega_nu = p->omega_xi = p->omega_1 = p->omega_high = 1.0;
+  p->world = 1;
+}
+
+int lbm_cuboid_buffer_bytes(const lbm_cuboid_params* p, int64_t* bytes) {
+  int rc = validate(p);
+  if (rc) return rc;
+  if (!bytes) return fail(LBM_EINVAL, "bytes is NULL");
+  const int64_t nzl = p->nz / p->world;
+  *bytes = int64_t(27) * p->nx * p->ny * (nzl + 2) * (p->precision == LBM_FP64 ? 8 : 4);
+  return LBM_OK;
+}
+
+int lbm_cuboid_halo_plan(const lbm_cuboid_params* p, int64_t out[8]) {
+  int rc = validate(p);
+  if (rc) return rc;
+  if (!out) return fail(LBM_EINVAL, "out is NULL");
+  const HaloPlan hp = make_plan(p);
+  out[0] = hp.ghost ? 1 : 0;
+  out[1] = hp.peer_up;
+  out[2] = hp.peer_down;
+  out[3] = hp.count;
+  out[4] = hp.send_up;
+  out[5] = hp.recv_dn;
+  out[6] = hp.send_dn;
+  out[7] = hp.recv_up;
+  return LBM_OK;
+}
+
+int lbm_cuboid_nccl_unique_id(void* out128) {
+  if (!out128) return fail(LBM_EINVAL, "out is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  return LBM_OK;
+}
+
+int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
+  if (!out) return fail(LBM_EINVAL, "out is NULL");
+  *out = nullptr;
+  int rc = validate(p);
+  if (rc) return rc;
+  lbm_cuboid* h = new (std::nothrow) lbm_cuboid();
+  if (!h) return fail(LBM_ENOMEM, "host allocation failed");
+  h->p = *p;
+  h->nzl = p->nz / p->world;
+  h->z0 = p->rank * h->nzl;
+  h->nxy = int64_t(p->nx) * p->ny;
+  h->plane = 27 * h->nxy;
+  h->elem = (p->precision == LBM_FP64) ? 8 : 4;
+  h->buf_elems = h->plane * (h->nzl + 2);
+  const HaloPlan hp = make_plan(p);
+  h->ghost = hp.ghost;
+  h->peer_up = hp.peer_up;
+  h->peer_down = hp.peer_down;
+  fill_consts(h);
+
+  auto bail = [&](int code) {
+    lbm_cuboid_destroy(h);
+    return code;
+  };
+  if ((rc = set_device(h))) return bail(rc);
+  if (p->stream) {
+    h->stream = (cudaStream_t)p->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(fail(LBM_ECUDA, "cudaStreamCreate failed"));
+    h->own_stream = true;
+  }
+  const size_t bytes = size_t(h->buf_elems) * h->elem;
+  if (p->buf_a || p->buf_b) {
+    if (!p->buf_a || !p->buf_b) return bail(fail(LBM_EINVAL, "buf_a and buf_b must both be given or both NULL"));
+    h->buf[0] = p->buf_a;
+    h->buf[1] = p->buf_b;
+  } else {
+    for (int i = 0; i < 2; ++i)
+      if (cudaMalloc(&h->buf[i], bytes) != cudaSuccess) {
+        cudaGetLastError();
+        return bail(fail(LBM_ENOMEM, "cudaMalloc(%zu) for a population buffer failed", bytes));
+      }
+    h->own_buf = true;
+  }
+  // ghost planes must hold finite values even when unused (wall faces)
+  for (int i = 0; i < 2; ++i)
+    if (cudaMemsetAsync(h->buf[i], 0, bytes, h->stream) != cudaSuccess)
+      return bail(fail(LBM_ECUDA, "cudaMemsetAsync failed"));
+  if (cudaMalloc(&h->d_check, 8 * sizeof(double)) != cudaSuccess) return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
+  if (h->ghost) {
+    if (!p->nccl_uid) return bail(fail(LBM_EINVAL, "nccl_uid is required for the NCCL ghost exchange"));
+    if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(LBM_ECUDA, "stream/event creation failed"));
+    ncclUniqueId id;
+    std::memcpy(&id, p->nccl_uid, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&h->comm, p->world, id, p->rank);
+    if (r != ncclSuccess) {
+      h->comm = nullptr;
+      return bail(fail(LBM_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+    }
+  }
+  if (cudaStreamSynchronize(h->stream) != cudaSuccess) return bail(fail(LBM_ECUDA, "initial sync failed"));
+  *out = h;
+  return LBM_OK;
+}
+
+int lbm_cuboid_init_fields_device(lbm_cuboid_t* h, const double* rho, const double* u) {
+  if (!h || !rho || !u) return fail(LBM_EINVAL, "NULL argument");
+  int rc = set_device(h);
+  if (rc) return rc;
+  if ((rc = wait_halo(h))) return rc;
+  if ((rc = run_init(h, rho, u, (long long)h->nzl * h->nxy, 0, h->nzl))) return rc;
+  return exchange(h, h->cur);
+}
+
+int lbm_cuboid_init_fields(lbm_cuboid_t* h, const double* rho, const double* u) {
+  if (!h || !rho || !u) return fail(LBM_EINVAL, "NULL argument");
+  int rc = set_device(h);
+  if (rc) return rc;
+  if ((rc = wait_halo(h))) return rc;
+  const int cp = chunk_planes(h, 4);
+  if ((rc = ensure_stage(h, size_t(4) * cp * h->nxy * sizeof(double)))) return rc;
+  for (int z = 0; z < h->nzl; z += cp) {
+    const int n = std::min(cp, h->nzl - z);
+    const size_t cnt = size_t(n) * h->nxy;
+    double* srho = h->stage;
+    double* su = h->stage + cnt;
+    CU(cudaMemcpyAsync(srho, rho + size_t(z) * h->nxy, cnt * 8, cudaMemcpyHostToDevice, h->stream));
+    CU(cudaMemcpy2DAsync(su, cnt * 8, u + size_t(z) * h->nxy, size_t(h->nzl) * h->nxy * 8, cnt * 8, 3,
+                         cudaMemcpyHostToDevice, h->stream));
+    if ((rc = run_init(h, srho, su, (long long)cnt, z, n))) return rc;
+  }
+  CU(cudaStreamSynchronize(h->stream));
+  return exchange(h, h->cur);
+}
+
+int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (nsteps < 0) return fail(LBM_EINVAL, "nsteps must be >= 0");
+  int rc = set_device(h);
+  if (rc) return rc;
+  for (int64_t t = 0; t < nsteps; ++t) {
+    void* src = h->buf[h->cur];
+    void* dst = h->buf[h->cur ^ 1];
+    if (!h->ghost) {
+      if ((rc = launch_cs(h, src, dst, 0, h->nzl, h->stream))) return rc;
+    } else {
+      if ((rc = wait_halo(h))) return rc;
+      // boundary planes first (critical path of the exchange) ...
+      if ((rc = launch_cs(h, src, dst, 0, 1, h->stream))) return rc;
+      if (h->nzl > 1 && (rc = launch_cs(h, src, dst, h->nzl - 1, 1, h->stream))) return rc;
+      if ((rc = exchange(h, h->cur ^ 1))) return rc;
+      // ... then the interior, overlapping the NCCL transfer
+      if ((rc = launch_cs(h, src, dst, 1, h->nzl - 2, h->stream))) return rc;
+    }
+    h->cur ^= 1;
+    h->steps++;
+  }
+  return LBM_OK;
+}
+
+int lbm_cuboid_sync(lbm_cuboid_t* h) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  int rc = set_device(h);
+  if (rc) return rc;
+  if ((rc = wait_halo(h))) return rc;
+  CU(cudaStreamSynchronize(h->stream));
+  if (h->comm_stream) CU(cudaStreamSynchronize(h->comm_stream));
+  return LBM_OK;
+}
+
+int lbm_cuboid_get_macroscopic_device(lbm_cuboid_t* h, double* rho, double* u) {
+  if (!h || !rho || !u) return fail(LBM_EINVAL, "NULL argument");
+  int rc = set_device(h);
+  if (rc) return rc;
+  return run_macro(h, rho, u, (long long)h->nzl * h->nxy, 0, h->nzl);
+}
+
+int lbm_cuboid_get_macroscopic(lbm_cuboid_t* h, double* rho, double* u) {
+  if (!h || !rho || !u) return fail(LBM_EINVAL, "NULL argument");
+  int rc = set_device(h);
+  if (rc) return rc;
+  const int cp = chunk_planes(h, 4);
+  if ((rc = ensure_stage(h, size_t(4) * cp * h->nxy * sizeof(double)))) return rc;
+  for (int z = 0; z < h->nzl; z += cp) {
+    const int n = std::min(cp, h->nzl - z);
+    const size_t cnt = size_t(n) * h->nxy;
+    double* srho = h->stage;
+    double* su = h->stage + cnt;
+    if ((rc = run_macro(h, srho, su, (long long)cnt, z, n))) return rc;
+    CU(cudaMemcpyAsync(rho + size_t(z) * h->nxy, srho, cnt * 8, cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaMemcpy2DAsync(u + size_t(z) * h->nxy, size_t(h->nzl) * h->nxy * 8, su, cnt * 8, cnt * 8, 3,
+                         cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+  }
+  return LBM_OK;
+}
+
+int lbm_cuboid_get_populations_planes(lbm_cuboid_t* h, int32_t z_begin, int32_t n_planes, double* f) {
+  if (!h || !f) return fail(LBM_EINVAL, "NULL argument");
+  if (z_begin < 0 || n_planes < 0 || z_begin + n_planes > h->nzl)
+    return fail(LBM_EINVAL, "planes [%d, %d) outside the local slab [0, %d)", z_begin, z_begin + n_planes, h->nzl);
+  int rc = set_device(h);
+  if (rc) return rc;
+  if (n_planes == 0) return LBM_OK;
+  const int cp = std::min(chunk_planes(h, 27), int(n_planes));
+  if ((rc = ensure_stage(h, size_t(27) * cp * h->nxy * sizeof(double)))) return rc;
+  for (int z = 0; z < n_planes; z += cp) {
+    const int n = std::min(cp, n_planes - z);
+    const size_t cnt = size_t(n) * h->nxy;
+    if (h->p.precision == LBM_FP64)
+      lbm::k_pack<double><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], h->stage, n,
+                                                                         h->c, z_begin + z);
+    else
+      lbm::k_pack<float><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], h->stage, n,
+                                                                        h->c, z_begin + z);
+    CU(cudaGetLastError());
+    h->launches++;
+    CU(cudaMemcpy2DAsync(f + size_t(z) * h->nxy, size_t(n_planes) * h->nxy * 8, h->stage, cnt * 8, cnt * 8, 27,
+                         cudaMemcpyDeviceToHost, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+  }
+  return LBM_OK;
+}
+
+int lbm_cuboid_get_populations(lbm_cuboid_t* h, double* f) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  return lbm_cuboid_get_populations_planes(h, 0, h->nzl, f);
+}
+
+int lbm_cuboid_set_populations(lbm_cuboid_t* h, const double* f) {
+  if (!h || !f) return fail(LBM_EINVAL, "NULL argument");
+  int rc = set_device(h);
+  if (rc) return rc;
+  if ((rc = wait_halo(h))) return rc;
+  const int cp = chunk_planes(h, 27);
+  if ((rc = ensure_stage(h, size_t(27) * cp * h->nxy * sizeof(double)))) return rc;
+  for (int z = 0; z < h->nzl; z += cp) {
+    const int n = std::min(cp, h->nzl - z);
+    const size_t cnt = size_t(n) * h->nxy;
+    CU(cudaMemcpy2DAsync(h->stage, cnt * 8, f + size_t(z) * h->nxy, size_t(h->nzl) * h->nxy * 8, cnt * 8, 27,
+                         cudaMemcpyHostToDevice, h->stream));
+    if (h->p.precision == LBM_FP64)
+      lbm::k_unpack<double><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>(h->stage, (double*)h->buf[h->cur], n,
+                                                                           h->c, z);
+    else
+      lbm::k_unpack<float><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>(h->stage, (float*)h->buf[h->cur], n,
+                                                                          h->c, z);
+    CU(cudaGetLastError());
+    h->launches++;
+    CU(cudaStreamSynchronize(h->stream));
+  }
+  return exchange(h, h->cur);
+}
+
+int lbm_cuboid_check(lbm_cuboid_t* h, double out[7]) {
+  if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
+  int rc = set_device(h);
+  if (rc) return rc;
+  CU(cudaMemsetAsync(h->d_check, 0, 8 * sizeof(double), h->stream));
+  dim3 g = grid_for(h, h->nzl);
+  if (h->p.precision == LBM_FP64)
+    lbm::k_check<double><<<g, lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], h->d_check, h->c);
+  else
+    lbm::k_check<float><<<g, lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], h->d_check, h->c);
+  CU(cudaGetLastError());
+  h->launches++;
+  CU(cudaMemcpyAsync(out, h->d_check, 7 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  if (out[6] > 0) return fail(LBM_EUNSTABLE, "%.0f nodes with NaN, rho <= 0 or |u| > 1 after %lld steps", out[6],
+                              (long long)h->steps);
+  return LBM_OK;
+}
+
+int lbm_cuboid_set_force(lbm_cuboid_t* h, const double force[3]) {
+  if (!h || !force) return fail(LBM_EINVAL, "NULL argument");
+  for (int d = 0; d < 3; ++d) {
+    if (!std::isfinite(force[d])) return fail(LBM_EINVAL, "force must be finite");
+    h->p.force[d] = force[d];
+    h->c.F[d] = force[d];
+  }
+  return LBM_OK;
+}
+
+int lbm_cuboid_info(const lbm_cuboid_t* h, int64_t out[8]) {
+  if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
+  out[0] = h->launches;
+  out[1] = h->cs_launches;
+  out[2] = h->steps;
+  out[3] = int64_t(2 * 27) * int64_t(h->elem);
+  out[4] = h->nxy * h->nzl;
+  out[5] = h->buf_elems * int64_t(h->elem);
+  out[6] = h->ghost ? 1 : 0;
+  out[7] = 0;
+  return LBM_OK;
+}
+
+void* lbm_cuboid_stream(const lbm_cuboid_t* h) { return h ? (void*)h->stream : nullptr; }
+
+int lbm_cuboid_destroy(lbm_cuboid_t* h) {
+  if (!h) return LBM_OK;
+  cudaSetDevice(h->p.device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
+  if (h->comm) ncclCommDestroy(h->comm);
+  if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
+  if (h->ev_halo) cudaEventDestroy(h->ev_halo);
+  if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
+  if (h->own_buf)
+    for (int i = 0; i < 2; ++i)
+      if (h->buf[i]) cudaFree(h->buf[i]);
+  if (h->stage) cudaFree(h->stage);
+  if (h->d_check) cudaFree(h->d_check);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return LBM_OK;
+}
+
+const char* lbm_cuboid_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

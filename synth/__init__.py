@@ -130,24 +130,29 @@ def slab_range(nz: int, rank: int, world: int) -> tuple[int, int]:
     return rank * n, (rank + 1) * n
 
 
-def tgv_fields(nx, ny, nz, cs2, u0, z0=0, z1=None, nz_global=None):
+def tgv_fields(nx, ny, nz, cs2, u0, z0=0, z1=None, nz_global=None, xp=np, device=None):
     """Decaying Taylor-Green vortex initial fields (reading R9):
     u = u0 (sin x cos y cos z, -cos x sin y cos z, 0) and
     rho = 1 + (u0^2/16)(cos 2x + cos 2y)(cos 2z + 2)/cs2, at node phases
     x = 2 pi i/nx, y = 2 pi j/ny, z = 2 pi k/nz_global.  Returns the slab
-    [z0, z1) of the global field."""
+    [z0, z1) of the global field.  xp = numpy (host arrays) or torch (arrays
+    on `device`, fp64, same values) for device-resident bench inputs."""
     nz_global = nz if nz_global is None else nz_global
     z1 = nz_global if z1 is None else z1
-    x = 2 * np.pi * np.arange(nx) / nx
-    y = 2 * np.pi * np.arange(ny) / ny
-    z = 2 * np.pi * np.arange(z0, z1) / nz_global
-    Z, Y, X = np.meshgrid(z, y, x, indexing="ij")
-    u = np.empty((3,) + X.shape)
-    u[0] = u0 * np.sin(X) * np.cos(Y) * np.cos(Z)
-    u[1] = -u0 * np.cos(X) * np.sin(Y) * np.cos(Z)
-    u[2] = 0.0
-    rho = 1.0 + (u0 * u0 / 16.0) * (np.cos(2 * X) + np.cos(2 * Y)) * (np.cos(2 * Z) + 2.0) / cs2
-    return np.ascontiguousarray(rho), np.ascontiguousarray(u)
+    kw = {} if xp is np else {"dtype": xp.float64, "device": device}
+    x = 2 * np.pi * xp.arange(nx, **kw) / nx
+    y = 2 * np.pi * xp.arange(ny, **kw) / ny
+    z = 2 * np.pi * xp.arange(z0, z1, **kw) / nz_global
+    X, Y, Z = x[None, None, :], y[None, :, None], z[:, None, None]
+    shape = (z1 - z0, ny, nx)
+    u = xp.zeros((3,) + shape, **kw)
+    u[0] = u0 * xp.sin(X) * xp.cos(Y) * xp.cos(Z)
+    u[1] = -u0 * xp.cos(X) * xp.sin(Y) * xp.cos(Z)
+    rho = 1.0 + (u0 * u0 / 16.0) * (xp.cos(2 * X) + xp.cos(2 * Y)) * (xp.cos(2 * Z) + 2.0) / cs2
+    rho = rho + xp.zeros(shape, **kw)
+    if xp is np:
+        return np.ascontiguousarray(rho), np.ascontiguousarray(u)
+    return rho.contiguous(), u.contiguous()
 
 
 def rest_fields(nx, ny, nz):

@@ -1,0 +1,279 @@
+"""GPU parity: the CUDA path (through the C ABI via the thin binding) against the
+CPU oracle, element by element, on the same seeded inputs.
+
+Tolerances: fp64 max|df| <= 1e-12 after 100 steps
+(BASELINE.json north_star); fp32 storage max |df|/|f| <= 1e-5 (reading R12).
+Sizes: small enough for the oracle (~0.6 MLUPS) to finish in seconds, chosen to
+span several 128-thread blocks with ragged tails (nx*ny not a multiple of 128).
+"""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2107_14774_b200 as P
+
+    P.load()
+    return P
+
+
+def _oracle(w):
+    import oracle as O
+
+    return O.Oracle(**w.params())
+
+
+def _gpu(P, w, **kw):
+    d = w.params()
+    d.update(kw)
+    return P.Lattice(**d)
+
+
+def _init_both(P, w, seed=None, noneq=0.0, **kw):
+    o = _oracle(w)
+    g = _gpu(P, w, **kw)
+    if seed is None:
+        rho, u = synth.initial_fields(w)
+    else:
+        rho, u = synth.random_fields(w.nx, w.ny, w.nz, seed)
+    o.init_fields(rho, u)
+    if noneq:
+        f = o.get_populations() * (1.0 + noneq * synth.noise((27, w.nz, w.ny, w.nx), 1000 + (seed or 0)))
+        o.set_populations(f)
+        g.set_populations(f)
+    else:
+        g.init_fields(rho, u)
+    return o, g
+
+
+def _cmp(o, g, prec=0):
+    fo = o.get_populations()
+    fg = g.get_populations()
+    assert np.all(np.isfinite(fg))
+    if prec == 0:
+        err = np.abs(fg - fo).max()
+        assert err <= TOL64, err
+    else:
+        err = (np.abs(fg - fo) / np.abs(fo)).max()
+        assert err <= TOL32, err
+    return err
+
+
+CASES = {
+    # name: (workload, reduced grid)
+    "tgv_full": synth.CONFIGS["tgv"],
+    "duct": synth.CONFIGS["duct"].scaled(nx=5, ny=37, nz=19),
+    "cavity100": synth.CONFIGS["cavity100"].scaled(nx=21, ny=19, nz=11),
+    "cavity1000": synth.CONFIGS["cavity1000"].scaled(nx=17, ny=23, nz=9),
+    "shear": synth.CONFIGS["shear"].scaled(nx=16, ny=29, nz=12),
+    "weak_tgv": synth.CONFIGS["weak"].scaled(nx=40, ny=24, nz=12),
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_parity_fp64_100_steps(P, name):
+    w = CASES[name]
+    o, g = _init_both(P, w, seed=7)
+    _cmp(o, g)  # initialisation (reading R8)
+    o.step(100)
+    g.step(100)
+    _cmp(o, g)
+
+
+@pytest.mark.parametrize("name", ["tgv_full", "cavity100", "shear", "duct"])
+def test_parity_fp32_storage(P, name):
+    w = CASES[name].scaled(precision=synth.PREC_FP32)
+    o, g = _init_both(P, w, seed=3)
+    # the GPU stores fp32: compare after the same 100 steps relative to the fp64 oracle
+    o.step(100)
+    g.step(100)
+    _cmp(o, g, prec=1)
+
+
+@pytest.mark.parametrize("corr", [synth.CORR_LOW_MACH, synth.CORR_OFF])
+def test_parity_correction_modes(P, corr):
+    w = CASES["weak_tgv"].scaled(corrections=corr)
+    o, g = _init_both(P, w, seed=11, noneq=1e-3)
+    o.step(50)
+    g.step(50)
+    _cmp(o, g)
+
+
+def test_parity_generic_rates_and_force(P):
+    """omega_1, omega_high != 1 (all App D relaxations active), body force, OFF-axis
+    aspect ratios."""
+    w = synth.Workload("generic", 19, 13, 10, r=0.75, s=1.3, nu=0.02, omega_xi=1.4, omega_1=1.2,
+                       omega_high=0.9, force=(2e-5, -1e-5, 5e-6), init="random", seed=5)
+    o, g = _init_both(P, w, seed=5, noneq=1e-3)
+    o.step(60)
+    g.step(60)
+    _cmp(o, g)
+
+
+def test_parity_nonequilibrium_walls(P):
+    """All wall kinds with a non-equilibrium start: moving lid + bounce-back box."""
+    w = CASES["cavity100"]
+    o, g = _init_both(P, w, seed=13, noneq=2e-3)
+    o.step(80)
+    g.step(80)
+    _cmp(o, g)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (1, 7, 5), (3, 1, 4), (6, 5, 1), (130, 1, 2)])
+def test_parity_degenerate_grids(P, shape):
+    """Degenerate extents (1 node along an axis wraps onto itself)."""
+    nx, ny, nz = shape
+    w = synth.CONFIGS["weak"].scaled(nx=nx, ny=ny, nz=nz, init="random")
+    o, g = _init_both(P, w, seed=17, noneq=1e-3)
+    o.step(30)
+    g.step(30)
+    _cmp(o, g)
+
+
+def test_parity_duct_walls_thin(P):
+    """Walls on both faces of a 1-node-thick axis (bounce-back twice per link)."""
+    w = synth.CONFIGS["duct"].scaled(nx=3, ny=1, nz=6)
+    o, g = _init_both(P, w, seed=19, noneq=1e-3)
+    o.step(30)
+    g.step(30)
+    _cmp(o, g)
+
+
+def test_nccl_self_halo_matches_wrap(P):
+    """LBM_HALO_NCCL on one GPU (send-to-self ghost planes) gives bitwise the
+    same result as the in-kernel z wrap."""
+    w = CASES["weak_tgv"]
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 23)
+    a = _gpu(P, w)
+    uid = P.nccl_unique_id()
+    b = _gpu(P, w, halo=P.HALO_NCCL, nccl_uid=uid)
+    assert b.info()["nccl_halo"] == 1 and a.info()["nccl_halo"] == 0
+    a.init_fields(rho, u)
+    b.init_fields(rho, u)
+    a.step(40)
+    b.step(40)
+    assert np.array_equal(a.get_populations(), b.get_populations())
+
+
+def test_zero_steps_and_roundtrips(P):
+    w = CASES["shear"]
+    g = _gpu(P, w)
+    rho, u = synth.initial_fields(w)
+    g.init_fields(rho, u)
+    r2, u2 = g.get_macroscopic()
+    assert np.abs(r2 - rho).max() < 1e-14 and np.abs(u2 - u).max() < 1e-15
+    f = g.get_populations()
+    g.step(0)
+    assert np.array_equal(f, g.get_populations())
+    f2 = f * (1 + 1e-3 * synth.noise(f.shape, 4))
+    g.set_populations(f2)
+    assert np.array_equal(f2, g.get_populations())
+    fp = g.get_populations_planes(3, 4)
+    assert np.array_equal(fp, f2[:, 3:7])
+
+
+def test_device_init_and_macroscopic(P):
+    import torch
+
+    w = CASES["weak_tgv"]
+    g = _gpu(P, w)
+    rho, u = synth.tgv_fields(w.nx, w.ny, w.nz, w.cs2_value, w.u0, xp=torch, device="cuda")
+    g.init_fields(rho, u)
+    g.step(5)
+    rd, ud = g.get_macroscopic(device=True)
+    torch.cuda.synchronize()
+    rh, uh = g.get_macroscopic()
+    assert np.array_equal(rd.cpu().numpy(), rh) and np.array_equal(ud.cpu().numpy(), uh)
+
+
+def test_conservation_and_check(P):
+    w = CASES["cavity1000"]
+    g = _gpu(P, w)
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 29, rho_amp=1e-3, u_amp=1e-3)
+    g.init_fields(rho, u)
+    m0 = g.check()["mass"]
+    g.step(300)
+    d = g.check()
+    assert abs(d["mass"] - m0) / m0 < 1e-12
+    assert d["bad_nodes"] == 0 and d["max_speed"] < 0.2
+    f = g.get_populations()
+    f[5, 1, 2, 3] = np.nan
+    g.set_populations(f)
+    with pytest.raises(P.LbmError):
+        g.check()
+
+
+def test_invalid_parameters_raise(P):
+    w = CASES["tgv_full"]
+    with pytest.raises(P.LbmError):
+        _gpu(P, w, omega_nu=2.5)
+    with pytest.raises(P.LbmError):
+        _gpu(P, w, bc=(2, 2, 0, 0, 0, 0))  # moving wall off the +y face
+    with pytest.raises(P.LbmError):
+        _gpu(P, w, cs2=1.5)
+
+
+def _tgv_patch_oracle(w, nx, ny, nz, xs, ys, zs):
+    """Oracle update of single nodes of the full-size periodic TGV after one
+    step: a 3x3x3 periodic patch of the initial fields around each node
+    reproduces exactly the node's 27 pull sources."""
+    import oracle as O
+
+    out = []
+    d = w.params()
+    d.update(nx=3, ny=3, nz=3)
+    o = O.Oracle(**d)
+    for x, y, z in zip(xs, ys, zs):
+        X = 2 * np.pi * (((x + np.arange(-1, 2)) % nx) / nx)
+        Y = 2 * np.pi * (((y + np.arange(-1, 2)) % ny) / ny)
+        Z = 2 * np.pi * (((z + np.arange(-1, 2)) % nz) / nz)
+        Zg, Yg, Xg = np.meshgrid(Z, Y, X, indexing="ij")
+        u = np.zeros((3, 3, 3, 3))
+        u[0] = w.u0 * np.sin(Xg) * np.cos(Yg) * np.cos(Zg)
+        u[1] = -w.u0 * np.cos(Xg) * np.sin(Yg) * np.cos(Zg)
+        rho = 1.0 + (w.u0 ** 2 / 16) * (np.cos(2 * Xg) + np.cos(2 * Yg)) * (np.cos(2 * Zg) + 2.0) / w.cs2_value
+        o.init_fields(rho, u)
+        o.step(1)
+        out.append(o.get_populations()[:, 1, 1, 1])
+    return np.array(out)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_full_size_bench_config_sampled(P, precision):
+    """BASELINE config 5 (weak, 512^3 per GPU, r=1, s=2) in the launch
+    configuration bench.py times: one step on the full grid, sampled nodes
+    (incl. all faces/edges/corners of the periodic box) against the oracle."""
+    import torch
+
+    w = synth.CONFIGS["weak"].scaled(precision=precision)
+    g = _gpu(P, w)
+    rho, u = synth.tgv_fields(w.nx, w.ny, w.nz, w.cs2_value, w.u0, xp=torch, device="cuda")
+    g.init_fields(rho, u)
+    del rho, u
+    g.step(1)
+    rng = np.random.default_rng(1)
+    planes = [0, 1, 255, 510, 511]
+    for z in planes:
+        fz = g.get_populations_planes(z, 1)[:, 0]
+        xs = np.concatenate([[0, w.nx - 1, 0, w.nx - 1], rng.integers(0, w.nx, 6)])
+        ys = np.concatenate([[0, 0, w.ny - 1, w.ny - 1], rng.integers(0, w.ny, 6)])
+        ref = _tgv_patch_oracle(w, w.nx, w.ny, w.nz, xs, ys, [z] * len(xs))
+        got = fz[:, ys, xs].T
+        if precision == 0:
+            assert np.abs(got - ref).max() <= TOL64
+        else:
+            assert (np.abs(got - ref) / np.abs(ref)).max() <= TOL32
+    d = g.check()
+    assert d["bad_nodes"] == 0
