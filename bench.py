@@ -39,7 +39,7 @@ METRIC = "D3Q27 cuboid CM-LBM MLUPS (fp64) at 1/2/4/8 B200; achieved roofline fr
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
     ap.add_argument("--workload", default="weak", choices=["weak", "shear", "cavity100", "cavity1000", "tgv"])
@@ -64,51 +64,61 @@ def workload(args, world):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi samples of SM clock and throttle reasons DURING the timed region."""
+    """`nvidia-smi -lms 100` running DURING the timed region (started before,
+    terminated after): median SM clock under load and throttle reasons seen."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw.instant,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
+    def __init__(self, index, log_path=None):
         self.index = index
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:  # noqa: BLE001
-                pass
-            self._stop.wait(0.2)
+        self.log_path = log_path
+        self.proc = None
+        self.out = ""
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let the sampler start before the timed region
+        except OSError:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=10)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+            if self.log_path:
+                with open(self.log_path, "w") as fh:
+                    fh.write(self.out)
 
     def summary(self):
-        if not self.samples:
+        rows = [[c.strip() for c in ln.split(",")] for ln in self.out.splitlines() if ln.count(",") >= 6]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        pw = [num(r[2]) for r in rows]
+        load = [r for r, p in zip(rows, pw) if p is not None and p > 350.0] or rows
+        sm = [num(r[0]) for r in load if num(r[0]) is not None]
+        mx = [num(r[1]) for r in rows if num(r[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and
-                          s[3 + i].lower().startswith("active")})
-        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for r in load for i in range(4) if r[3 + i].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples),
-                "power_w_max": max(pw) if pw else None}
+                "reasons": reasons, "samples": len(rows), "samples_under_load": len(load),
+                "power_w_max": max(p for p in pw if p is not None) if any(p is not None for p in pw) else None}
 
 
 def measured_peaks():
@@ -237,27 +247,32 @@ def run_cuda(args):
         lat.step(args.warmup)
     barrier()
 
-    # ---- timed region: K steps, one event pair per step on the compute stream
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    # ---- timed region: exactly K steps between barrier+sync, one event pair on the compute stream
     l0 = lat.info()["launches"]
-    with ClockSampler(local) as clk:
+    with ClockSampler(local, os.path.join(ROOT, "gpurun_out", f"bench_clocks_rank{rank}.csv")
+                      if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else None) as clk:
         barrier()
         t_start = torch.cuda.Event(enable_timing=True)
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
-        for i in range(args.steps):
-            ev[i][0].record(stream)
-            lat.step(1)
-            ev[i][1].record(stream)
+        lat.step(args.steps)
         t_end.record(stream)
         barrier()
     launches = lat.info()["launches"] - l0
     elapsed_ms = max_over_ranks(t_start.elapsed_time(t_end))
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    kernel_ms = float(np.mean(step_ms))
-    bad = lat.check(raise_on_unstable=False)["bad_nodes"]
     mlups = w.nodes * args.steps / (elapsed_ms * 1e-3) / 1e6
     bpn = lat.info()["bytes_per_node_update"]
+
+    # ---- dominant-kernel duration: the same K steps again with the library's
+    # per-launch CUDA events on the compute stream (kept out of the timed region)
+    lat.timing(True)
+    lat.step(args.steps)
+    tk = lat.timing_read()
+    lat.timing(False)
+    barrier()
+    kernel_ms = tk["kernel_ms"] / max(tk["launches"], 1)
+    nodes_per_launch = tk["node_updates"] / max(tk["launches"], 1)
+    bad = lat.check(raise_on_unstable=False)["bad_nodes"]
 
     # ---- e2e through the C ABI with host buffers
     e2e = None
@@ -296,16 +311,18 @@ def run_cuda(args):
         return
 
     peak, peak_src = measured_peaks()
-    achieved = bpn * nloc / (kernel_ms * 1e-3) / 1e9
+    achieved = bpn * nodes_per_launch / (kernel_ms * 1e-3) / 1e9
     prec = "fp64" if w.precision == 0 else "fp32"
     traffic = ncu_traffic(w.name, prec)
+    kname = "k_collide_stream_paper" if lat.info()["paper_rate_kernel"] else "k_collide_stream"
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src,
-            "kernel": "k_collide_stream<double>" if prec == "fp64" else "k_collide_stream<float>",
-            "bytes_per_node": bpn, "nodes_per_launch": nloc if world == 1 else None,
-            "kernel_ms_mean": kernel_ms,
-            "note": "algorithmic bytes 2*27*sizeof(real) per node / mean per-step duration (1 launch per step "
-                    "at N=1; at N>1 the step also holds the boundary-plane launches and the NCCL halo)"}
+            "kernel": f"{kname}<{'double' if prec == 'fp64' else 'float'}>",
+            "bytes_per_node": bpn, "nodes_per_launch": nodes_per_launch, "kernel_ms_mean": kernel_ms,
+            "launches_timed": tk["launches"],
+            "note": "achieved = 2*27*sizeof(real) B/node x nodes per launch / mean launch duration (library "
+                    "CUDA events around each collide-stream launch on the compute stream, K steps after the "
+                    "timed region; at N>1 a step has 2 launches: boundary planes + interior)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, n, ws = oracle_mlups(w, budget_s=12.0)

@@ -182,6 +182,15 @@ int lbm_cuboid_info(const lbm_cuboid_t *h, int64_t out[8]);
 /* cudaStream_t of the compute stream (for event timing by the caller). */
 void *lbm_cuboid_stream(const lbm_cuboid_t *h);
 
+/* Per-launch timing of the collide-stream kernel: while enabled, every launch
+ * is bracketed by a CUDA event pair on the compute stream (at most 65536
+ * launches are recorded).  lbm_cuboid_timing() synchronises and clears the
+ * record; lbm_cuboid_timing_read() synchronises and returns
+ * out[0] = launches recorded, out[1] = their summed duration in ms,
+ * out[2] = node updates they performed. */
+int lbm_cuboid_timing(lbm_cuboid_t *h, int enable);
+int lbm_cuboid_timing_read(lbm_cuboid_t *h, double out[3]);
+
 /* Release library state (streams, events, NCCL comm, library-owned buffers).
  * Caller-owned buffers are untouched.  NULL is accepted. */
 int lbm_cuboid_destroy(lbm_cuboid_t *h);

@@ -40,25 +40,27 @@ def needs_build() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile liblbm_cuboid.so (or, with out/defines, a kernel variant)."""
+    target = out or LIB
+    if out is None and not force and not needs_build():
         return LIB
     inc, libdir = nccl_dirs()
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = target + f".tmp{os.getpid()}"
     cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "-shared",
            "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-I", inc,
-           os.path.join(CSRC, "lbm_cuboid.cu"), "-o", tmp,
+           *[f"-D{d}" for d in defines], os.path.join(CSRC, "lbm_cuboid.cu"), "-o", tmp,
            "-L", libdir, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{libdir}"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building liblbm_cuboid.so")
-    with open(os.path.join(PKG, "ptxas.log"), "w") as fh:
+    with open(target + ".ptxas.log" if out else os.path.join(PKG, "ptxas.log"), "w") as fh:
         fh.write(res.stderr)
     if verbose:
         sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -20,7 +20,19 @@
 
 namespace lbm {
 
-constexpr int kBlock = 128;  // threads per block (one node per thread)
+#ifndef LBM_BLOCK
+#define LBM_BLOCK 128
+#endif
+#ifndef LBM_MINB
+#define LBM_MINB 0  // min resident blocks per SM for __launch_bounds__ (0: none)
+#endif
+#ifndef LBM_LDMODE
+#define LBM_LDMODE 0  // 0: ld.global.nc; 1: ld.global.nc.L1::no_allocate
+#endif
+#ifndef LBM_STMODE
+#define LBM_STMODE 0  // 0: st.global.cs (evict-first); 1: plain st.global
+#endif
+constexpr int kBlock = LBM_BLOCK;  // threads per block (one node per thread)
 
 // local face treatment (per rank; z faces depend on the slab position)
 enum FaceKind : int {
@@ -53,12 +65,30 @@ struct Consts {
 
 // ------------------------------------------------------------------ memory ops
 template <typename T> __device__ __forceinline__ double ldg(const T* p);
+#if LBM_LDMODE == 1
+template <> __device__ __forceinline__ double ldg<double>(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+template <> __device__ __forceinline__ double ldg<float>(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return (double)v;
+}
+#else
 template <> __device__ __forceinline__ double ldg<double>(const double* p) { return __ldg(p); }
 template <> __device__ __forceinline__ double ldg<float>(const float* p) { return (double)__ldg(p); }
+#endif
 
 template <typename T> __device__ __forceinline__ void stcs(T* p, double v);
+#if LBM_STMODE == 1
+template <> __device__ __forceinline__ void stcs<double>(double* p, double v) { *p = v; }
+template <> __device__ __forceinline__ void stcs<float>(float* p, double v) { *p = (float)v; }
+#else
 template <> __device__ __forceinline__ void stcs<double>(double* p, double v) { __stcs(p, v); }
 template <> __device__ __forceinline__ void stcs<float>(float* p, double v) { __stcs(p, (float)v); }
+#endif
 
 #define LBM_Q(i, j, k) ((i) + 3 * (j) + 9 * (k))
 
@@ -293,15 +323,20 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
 }
 
 // --------------------------------------------------------- the fused kernel
-// One thread per node of planes [zbeg, zbeg + gridDim.y) of the local slab.
+// One thread per node of planes zbeg + i*zstride, i < gridDim.y, of the local slab.
+#if LBM_MINB > 0
+#define LBM_CS_BOUNDS __launch_bounds__(kBlock, LBM_MINB)
+#else
+#define LBM_CS_BOUNDS __launch_bounds__(kBlock)
+#endif
 template <typename T>
-__global__ void __launch_bounds__(kBlock) k_collide_stream(const T* __restrict__ src, T* __restrict__ dst,
-                                                           const __grid_constant__ Consts c, int zbeg) {
+__global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __restrict__ dst,
+                                                           const __grid_constant__ Consts c, int zbeg, int zstride) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
   const int y = idx / c.nx;
   const int x = idx - y * c.nx;
-  const int z = zbeg + blockIdx.y;
+  const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
 
   double f[27];
   gather<T>(src, c, x, y, z, f);
@@ -331,6 +366,128 @@ __global__ void __launch_bounds__(kBlock) k_collide_stream(const T* __restrict__
   T* out = dst + (long long)(z + 1) * c.plane + idx;
 #pragma unroll
   for (int q = 0; q < 27; ++q) stcs<T>(out + q * c.nxy, f[q]);
+}
+
+// ------------------------------------- paper-rate kernel (omega_1 = omega_high = 1)
+// With every rate except omega_nu and omega_xi equal to 1 (the setting
+// of all the paper's results), App D sends every first-order central moment to
+// F/2 (k~ = k + 1 (0 - k) + (1 - 1/2) F) and every moment of order >= 3 to its
+// equilibrium of Eq. 64 (0, cs^4 rho or cs^6 rho), whatever its pre-collision
+// value.  So the forward transform only needs the raw moments up to second
+// order, and the post-collision central moments are
+//   K000 = rho, K100 = Fx/2, K010 = Fy/2, K001 = Fz/2,
+//   K110, K101, K011 (relaxed with omega_nu), K200, K020, K002 (App D, B/B^-1),
+//   K220 = K202 = K022 = cs^4 rho, K222 = cs^6 rho, all others 0,
+// which the inverse per-axis transforms exploit (zero inputs skipped).
+
+// 1D inverse transform (central -> raw -> unscale -> populations), with
+// compile-time knowledge of zero inputs k1 / k2 (see inverse_pass).
+template <bool H1, bool H2>
+__device__ __forceinline__ void inv1d(double k0, double k1, double k2, double u, double h1, double h2,
+                                      double& fm, double& f0, double& fp) {
+  const double A = H1 ? fma(u, k0, k1) : u * k0;
+  const double t = H1 ? k1 + A : A;
+  const double B = H2 ? fma(u, t, k2) : u * t;
+  const double t1 = A * h1, t2 = B * h2;
+  fm = t2 - t1;
+  f0 = fma(-2.0, t2, k0);
+  fp = t2 + t1;
+}
+
+template <typename T>
+__global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, T* __restrict__ dst,
+                                                     const __grid_constant__ Consts c, int zbeg, int zstride) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int y = idx / c.nx;
+  const int x = idx - y * c.nx;
+  const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
+
+  double f[27];
+  gather<T>(src, c, x, y, z, f);
+
+  // raw moments up to second order, cubic units (App A restricted to m+n+p <= 2).
+  // x-pass on all nine (y,z) rows: slots (0,j,k), (1,j,k), (2,j,k) <- m0, m1, m2 along x
+  raw_pass<0>(f);
+  // y-pass: x-order 0 needs (m0, m1, m2); x-order 1 needs (m0, m1); x-order 2 needs m0
+  double a0[3], a1[3], a2[3], b0[3], b1[3], c0[3];  // [z slot]
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    {
+      const double fm = f[LBM_Q(0, 0, k)], f0 = f[LBM_Q(0, 1, k)], fp = f[LBM_Q(0, 2, k)];
+      const double sp = fp + fm;
+      a0[k] = sp + f0;
+      a1[k] = fp - fm;
+      a2[k] = sp;
+    }
+    {
+      const double fm = f[LBM_Q(1, 0, k)], f0 = f[LBM_Q(1, 1, k)], fp = f[LBM_Q(1, 2, k)];
+      b0[k] = (fp + fm) + f0;
+      b1[k] = fp - fm;
+    }
+    c0[k] = (f[LBM_Q(2, 0, k)] + f[LBM_Q(2, 2, k)]) + f[LBM_Q(2, 1, k)];
+  }
+  // z-pass
+  const double rho = (a0[2] + a0[0]) + a0[1];  // M000
+  const double Mz = a0[2] - a0[0];             // M001
+  const double Mzz = a0[2] + a0[0];            // M002
+  const double My = (a1[2] + a1[0]) + a1[1];   // M010
+  const double Myz = a1[2] - a1[0];            // M011
+  const double Myy = (a2[2] + a2[0]) + a2[1];  // M020
+  const double Mx = (b0[2] + b0[0]) + b0[1];   // M100
+  const double Mxz = b0[2] - b0[0];            // M101
+  const double Mxy = (b1[2] + b1[0]) + b1[1];  // M110
+  const double Mxx = (c0[2] + c0[0]) + c0[1];  // M200
+
+  // scale to the cuboid lattice (App B) and shift to central moments (App C)
+  const double inv_rho = 1.0 / rho;
+  const double jx = Mx, jy = c.r * My, jz = c.s * Mz;
+  const double ux = (jx + 0.5 * c.F[0]) * inv_rho;
+  const double uy = (jy + 0.5 * c.F[1]) * inv_rho;
+  const double uz = (jz + 0.5 * c.F[2]) * inv_rho;
+  // k_ab = Pi_ab - u_a j_b - u_b j_a + rho u_a u_b
+  const double k200 = Mxx - ux * fma(-rho, ux, 2.0 * jx);
+  const double k020 = fma(c.r2, Myy, -uy * fma(-rho, uy, 2.0 * jy));
+  const double k002 = fma(c.s2, Mzz, -uz * fma(-rho, uz, 2.0 * jz));
+  const double k110 = fma(c.r, Mxy, -fma(ux, jy, uy * fma(-rho, ux, jx)));
+  const double k101 = fma(c.s, Mxz, -fma(ux, jz, uz * fma(-rho, ux, jx)));
+  const double k011 = fma(c.r * c.s, Myz, -fma(uy, jz, uz * fma(-rho, uy, jy)));
+
+  // collision (App D) for the second order; first order -> F/2, higher -> Eq. 64
+  double K200, K020, K002;
+  second_order_diag(c, rho, inv_rho, ux, uy, uz, k200, k020, k002, K200, K020, K002);
+  const double om = 1.0 - c.wn;
+  const double K110 = om * k110, K101 = om * k101, K011 = om * k011;
+  const double K100 = 0.5 * c.F[0], K010 = 0.5 * c.F[1], K001 = 0.5 * c.F[2];
+  const double c4r = c.c4 * rho, c6r = c.c6 * rho;
+
+  // inverse transforms (App E, F, G per axis), z first.  G[i][j][kz]
+  double G00[3], G10[3], G01[3], G11[3], G20[3], G02[3], G22[3];
+  inv1d<true, true>(rho, K001, K002, uz, c.h1z, c.h2z, G00[0], G00[1], G00[2]);
+  inv1d<true, false>(K100, K101, 0.0, uz, c.h1z, c.h2z, G10[0], G10[1], G10[2]);
+  inv1d<true, false>(K010, K011, 0.0, uz, c.h1z, c.h2z, G01[0], G01[1], G01[2]);
+  inv1d<false, false>(K110, 0.0, 0.0, uz, c.h1z, c.h2z, G11[0], G11[1], G11[2]);
+  inv1d<false, true>(K200, 0.0, c4r, uz, c.h1z, c.h2z, G20[0], G20[1], G20[2]);
+  inv1d<false, true>(K020, 0.0, c4r, uz, c.h1z, c.h2z, G02[0], G02[1], G02[2]);
+  inv1d<false, true>(c4r, 0.0, c6r, uz, c.h1z, c.h2z, G22[0], G22[1], G22[2]);
+
+  T* out = dst + (long long)(z + 1) * c.plane + idx;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    // y: (x-order 0): (G00, G01, G02); (x-order 1): (G10, G11, 0); (x-order 2): (G20, 0, G22)
+    double H0[3], H1[3], H2[3];  // [jy] for x-orders 0, 1, 2
+    inv1d<true, true>(G00[k], G01[k], G02[k], uy, c.h1y, c.h2y, H0[0], H0[1], H0[2]);
+    inv1d<true, false>(G10[k], G11[k], 0.0, uy, c.h1y, c.h2y, H1[0], H1[1], H1[2]);
+    inv1d<false, true>(G20[k], 0.0, G22[k], uy, c.h1y, c.h2y, H2[0], H2[1], H2[2]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double fm, f0, fp;
+      inv1d<true, true>(H0[j], H1[j], H2[j], ux, 0.5, 0.5, fm, f0, fp);
+      stcs<T>(out + LBM_Q(0, j, k) * c.nxy, fm);
+      stcs<T>(out + LBM_Q(1, j, k) * c.nxy, f0);
+      stcs<T>(out + LBM_Q(2, j, k) * c.nxy, fp);
+    }
+  }
 }
 
 // -------------------------------------------------------------- init kernel

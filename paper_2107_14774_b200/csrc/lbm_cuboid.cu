@@ -55,6 +55,7 @@ int fail(int code, const char* fmt, ...) {
   } while (0)
 
 constexpr size_t kStageBytes = size_t(256) << 20;  // host<->device staging chunk
+constexpr size_t kMaxTimedLaunches = 1 << 16;
 
 }  // namespace
 
@@ -71,6 +72,7 @@ struct lbm_cuboid {
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   bool halo_pending = false;
   bool ghost = false;  // ghost-plane (NCCL) mode
+  bool paper_rates = false;  // omega_1 = omega_high = 1 -> k_collide_stream_paper
   ncclComm_t comm = nullptr;
   int peer_down = -1, peer_up = -1;  // ranks owning the planes below / above, -1 none
   Consts c{};
@@ -78,6 +80,10 @@ struct lbm_cuboid {
   size_t stage_bytes = 0;
   double* d_check = nullptr;
   int64_t launches = 0, cs_launches = 0, steps = 0;
+  // optional per-launch timing of the collide-stream kernel (lbm_cuboid_timing)
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_t;
+  std::vector<int64_t> ev_t_nodes;
 };
 
 namespace {
@@ -189,14 +195,36 @@ dim3 grid_for(const lbm_cuboid* h, int nplanes) {
   return dim3(unsigned((h->nxy + lbm::kBlock - 1) / lbm::kBlock), unsigned(nplanes), 1);
 }
 
-int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, cudaStream_t s) {
+int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, int zstride, cudaStream_t s) {
   if (nplanes <= 0) return LBM_OK;
   dim3 g = grid_for(h, nplanes);
-  if (h->p.precision == LBM_FP64)
-    lbm::k_collide_stream<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg);
-  else
-    lbm::k_collide_stream<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg);
+  const bool fp64 = (h->p.precision == LBM_FP64);
+  const bool timed = h->timing && h->ev_t.size() < kMaxTimedLaunches;
+  if (timed) {
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    h->ev_t.push_back({a, b});
+    CU(cudaEventRecord(a, s));
+  }
+  if (h->paper_rates) {
+    if (fp64)
+      lbm::k_collide_stream_paper<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg,
+                                                                    zstride);
+    else
+      lbm::k_collide_stream_paper<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg,
+                                                                   zstride);
+  } else {
+    if (fp64)
+      lbm::k_collide_stream<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg, zstride);
+    else
+      lbm::k_collide_stream<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg, zstride);
+  }
   CU(cudaGetLastError());
+  if (timed) {
+    CU(cudaEventRecord(h->ev_t.back().second, s));
+    h->ev_t_nodes.push_back(int64_t(nplanes) * h->nxy);
+  }
   h->launches++;
   h->cs_launches++;
   return LBM_OK;
@@ -373,6 +401,7 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->ghost = hp.ghost;
   h->peer_up = hp.peer_up;
   h->peer_down = hp.peer_down;
+  h->paper_rates = (p->omega_1 == 1.0 && p->omega_high == 1.0);
   fill_consts(h);
 
   auto bail = [&](int code) {
@@ -463,15 +492,15 @@ int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
     void* src = h->buf[h->cur];
     void* dst = h->buf[h->cur ^ 1];
     if (!h->ghost) {
-      if ((rc = launch_cs(h, src, dst, 0, h->nzl, h->stream))) return rc;
+      if ((rc = launch_cs(h, src, dst, 0, h->nzl, 1, h->stream))) return rc;
     } else {
       if ((rc = wait_halo(h))) return rc;
-      // boundary planes first (critical path of the exchange) ...
-      if ((rc = launch_cs(h, src, dst, 0, 1, h->stream))) return rc;
-      if (h->nzl > 1 && (rc = launch_cs(h, src, dst, h->nzl - 1, 1, h->stream))) return rc;
+      // both boundary planes first, in one launch (critical path of the exchange) ...
+      const int nb = (h->nzl > 1) ? 2 : 1;
+      if ((rc = launch_cs(h, src, dst, 0, nb, std::max(1, h->nzl - 1), h->stream))) return rc;
       if ((rc = exchange(h, h->cur ^ 1))) return rc;
       // ... then the interior, overlapping the NCCL transfer
-      if ((rc = launch_cs(h, src, dst, 1, h->nzl - 2, h->stream))) return rc;
+      if ((rc = launch_cs(h, src, dst, 1, h->nzl - 2, 1, h->stream))) return rc;
     }
     h->cur ^= 1;
     h->steps++;
@@ -611,11 +640,49 @@ int lbm_cuboid_info(const lbm_cuboid_t* h, int64_t out[8]) {
   out[4] = h->nxy * h->nzl;
   out[5] = h->buf_elems * int64_t(h->elem);
   out[6] = h->ghost ? 1 : 0;
-  out[7] = 0;
+  out[7] = h->paper_rates ? 1 : 0;
   return LBM_OK;
 }
 
 void* lbm_cuboid_stream(const lbm_cuboid_t* h) { return h ? (void*)h->stream : nullptr; }
+
+static void clear_timing(lbm_cuboid_t* h) {
+  for (auto& e : h->ev_t) {
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  h->ev_t.clear();
+  h->ev_t_nodes.clear();
+}
+
+int lbm_cuboid_timing(lbm_cuboid_t* h, int enable) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  int rc = set_device(h);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(h->stream));
+  clear_timing(h);
+  h->timing = (enable != 0);
+  return LBM_OK;
+}
+
+int lbm_cuboid_timing_read(lbm_cuboid_t* h, double out[3]) {
+  if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
+  int rc = set_device(h);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(h->stream));
+  double ms = 0.0;
+  int64_t nodes = 0;
+  for (size_t i = 0; i < h->ev_t.size(); ++i) {
+    float t = 0.f;
+    CU(cudaEventElapsedTime(&t, h->ev_t[i].first, h->ev_t[i].second));
+    ms += t;
+    nodes += h->ev_t_nodes[i];
+  }
+  out[0] = double(h->ev_t.size());
+  out[1] = ms;
+  out[2] = double(nodes);
+  return LBM_OK;
+}
 
 int lbm_cuboid_destroy(lbm_cuboid_t* h) {
   if (!h) return LBM_OK;
@@ -631,6 +698,7 @@ int lbm_cuboid_destroy(lbm_cuboid_t* h) {
       if (h->buf[i]) cudaFree(h->buf[i]);
   if (h->stage) cudaFree(h->stage);
   if (h->d_check) cudaFree(h->d_check);
+  clear_timing(h);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return LBM_OK;

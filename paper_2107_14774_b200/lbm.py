@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "liblbm_cuboid.so")
+# LBM_CUBOID_LIB selects an alternative build (kernel-variant sweeps); default in-tree
+LIB_PATH = os.environ.get("LBM_CUBOID_LIB", os.path.join(_PKG, "liblbm_cuboid.so"))
 
 LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EUNSTABLE, LBM_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
 BC_PERIODIC, BC_BOUNCE_BACK, BC_MOVING_WALL, BC_FREE_SLIP = 0, 1, 2, 3
@@ -30,7 +31,8 @@ EXPORTS = ["lbm_cuboid_default_params", "lbm_cuboid_buffer_bytes", "lbm_cuboid_h
            "lbm_cuboid_step", "lbm_cuboid_sync", "lbm_cuboid_get_macroscopic",
            "lbm_cuboid_get_macroscopic_device", "lbm_cuboid_get_populations",
            "lbm_cuboid_get_populations_planes", "lbm_cuboid_set_populations", "lbm_cuboid_check", "lbm_cuboid_set_force",
-           "lbm_cuboid_info", "lbm_cuboid_stream", "lbm_cuboid_destroy", "lbm_cuboid_last_error"]
+           "lbm_cuboid_info", "lbm_cuboid_stream", "lbm_cuboid_timing", "lbm_cuboid_timing_read",
+           "lbm_cuboid_destroy", "lbm_cuboid_last_error"]
 
 
 class LbmError(RuntimeError):
@@ -85,6 +87,8 @@ def load():
     L.lbm_cuboid_info.argtypes = [_VP, ctypes.POINTER(ctypes.c_int64)]
     L.lbm_cuboid_stream.argtypes = [_VP]
     L.lbm_cuboid_stream.restype = _VP
+    L.lbm_cuboid_timing.argtypes = [_VP, ctypes.c_int]
+    L.lbm_cuboid_timing_read.argtypes = [_VP, _D]
     L.lbm_cuboid_destroy.argtypes = [_VP]
     L.lbm_cuboid_last_error.argtypes = []
     L.lbm_cuboid_last_error.restype = ctypes.c_char_p
@@ -95,7 +99,8 @@ def load():
               "lbm_cuboid_sync", "lbm_cuboid_get_macroscopic", "lbm_cuboid_get_macroscopic_device",
               "lbm_cuboid_get_populations", "lbm_cuboid_get_populations_planes",
               "lbm_cuboid_set_populations", "lbm_cuboid_check",
-              "lbm_cuboid_set_force", "lbm_cuboid_info", "lbm_cuboid_destroy"):
+              "lbm_cuboid_set_force", "lbm_cuboid_info", "lbm_cuboid_timing", "lbm_cuboid_timing_read",
+              "lbm_cuboid_destroy"):
         getattr(L, n).restype = ctypes.c_int
     _lib = L
     return L
@@ -275,6 +280,15 @@ class Lattice:
         keys = ["launches", "collide_stream_launches", "steps", "bytes_per_node_update",
                 "local_nodes", "buffer_bytes", "nccl_halo", "paper_rate_kernel"]
         return dict(zip(keys, list(a)))
+
+    def timing(self, enable: bool):
+        """Enable/disable (and clear) per-launch CUDA-event timing of the collide-stream kernel."""
+        _check(load().lbm_cuboid_timing(self._h, 1 if enable else 0))
+
+    def timing_read(self):
+        a = np.zeros(3)
+        _check(load().lbm_cuboid_timing_read(self._h, a.ctypes.data_as(_D)))
+        return {"launches": int(a[0]), "kernel_ms": float(a[1]), "node_updates": int(a[2])}
 
     def close(self):
         if getattr(self, "_h", None):
