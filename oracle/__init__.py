@@ -37,7 +37,7 @@ class _Params(ctypes.Structure):
                 ("omega_nu", ctypes.c_double), ("omega_xi", ctypes.c_double),
                 ("omega_1", ctypes.c_double), ("omega_high", ctypes.c_double),
                 ("force", ctypes.c_double * 3), ("bc", ctypes.c_int32 * 6),
-                ("wall_u", ctypes.c_double), ("corrections", ctypes.c_int32)]
+                ("wall_u", ctypes.c_double), ("corrections", ctypes.c_int32), ("model", ctypes.c_int32)]
 
 
 _lib = None
@@ -64,6 +64,8 @@ def lib():
         L.oracle_raw_equilibria.argtypes = [ctypes.c_double, _D, ctypes.c_double, _D]
         L.oracle_feq.argtypes = [ctypes.c_void_p, ctypes.c_double, _D, _D]
         L.oracle_collide.argtypes = [ctypes.c_void_p, _D, _D]
+        L.oracle_collide_raw.argtypes = [ctypes.c_void_p, _D, _D]
+        L.oracle_raw_source.argtypes = [_D, _D, _D]
         L.oracle_lid_term.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_double]
         L.oracle_lid_term.restype = ctypes.c_double
         L.oracle_step.argtypes = [ctypes.c_void_p, _D, _D]
@@ -134,6 +136,12 @@ def frame(m, a):
     return out
 
 
+def raw_source(u, F):
+    phi = np.zeros(27)
+    lib().oracle_raw_source(_p(_arr(u, 3)), _p(_arr(F, 3)), _p(phi))
+    return phi
+
+
 def raw_equilibria(rho, u, cs2):
     m = np.zeros(27)
     lib().oracle_raw_equilibria(float(rho), _p(_arr(u, 3)), float(cs2), _p(m))
@@ -147,8 +155,8 @@ class Oracle:
 
     def __init__(self, nx, ny, nz, r, s, cs2, omega_nu, omega_xi=1.0, omega_1=1.0,
                  omega_high=1.0, force=(0.0, 0.0, 0.0), bc=(0,) * 6, wall_u=0.0,
-                 corrections=0, precision=0):
-        del precision  # the oracle is always fp64
+                 corrections=0, precision=0, model=0, **ignored):
+        del precision, ignored  # the oracle is always fp64; GPU-only knobs (halo, graphs, ...) ignored
         p = _Params()
         p.nx, p.ny, p.nz = nx, ny, nz
         p.r, p.s, p.cs2 = r, s, cs2
@@ -159,6 +167,8 @@ class Oracle:
             p.bc[i] = bc[i]
         p.wall_u = wall_u
         p.corrections = corrections
+        p.model = model
+        self.model = model
         self._params = p
         self.shape = (nz, ny, nx)
         self.nx, self.ny, self.nz = nx, ny, nz
@@ -191,7 +201,8 @@ class Oracle:
 
     def collide(self, f):
         out = np.zeros(27)
-        lib().oracle_collide(self._ctx, _p(_arr(f, 27)), _p(out))
+        fn = lib().oracle_collide_raw if self.model == 1 else lib().oracle_collide
+        fn(self._ctx, _p(_arr(f, 27)), _p(out))
         return out
 
     def lid_term(self, q, rho_f):

@@ -19,6 +19,7 @@
  *   raw equilibria      Eq. 10, literally
  *   collision           App D: B, effective equilibria, local
  *                       strain rates, relax, B^-1
+ *   3DCRM variant       raw-moment collision, Eq. 10/11          P:L642-648, L744(ii), L1011
  *   central -> raw      binomial transform F^-1 = F(-u)
  *   post-coll. f        f~ = Q^-1 m~  (= P^-1 S^-1 m~)
  *   streaming           pull form f(x,t+1) = f~(x - e, t)
@@ -75,6 +76,7 @@ typedef struct {
   int32_t bc[6]; /* faces -x,+x,-y,+y,-z,+z */
   double wall_u; /* +y face moves with velocity (U,0,0) */
   int32_t corrections;
+  int32_t model; /* 0: 3DCCM (central moments); 1: 3DCRM (raw moments) */
 } oracle_params;
 
 typedef struct {
@@ -381,6 +383,126 @@ void oracle_collide(const oracle_ctx *c, const double *f, double *ft) {
   matvec(c->Qinv, mt, ft);
 }
 
+/* Eq. 11: raw moments of the source term, zero from third order on. */
+void oracle_raw_source(const double *u, const double *F, double *phi) {
+  for (int j = 0; j < NQ; ++j) phi[j] = 0.0;
+  phi[midx(1, 0, 0)] = F[0];
+  phi[midx(0, 1, 0)] = F[1];
+  phi[midx(0, 0, 1)] = F[2];
+  phi[midx(1, 1, 0)] = F[0] * u[1] + F[1] * u[0];
+  phi[midx(1, 0, 1)] = F[0] * u[2] + F[2] * u[0];
+  phi[midx(0, 1, 1)] = F[1] * u[2] + F[2] * u[1];
+  phi[midx(2, 0, 0)] = 2.0 * F[0] * u[0];
+  phi[midx(0, 2, 0)] = 2.0 * F[1] * u[1];
+  phi[midx(0, 0, 2)] = 2.0 * F[2] * u[2];
+}
+
+/* 3DCRM-LBM (P:L1011 and remark (ii) of P:L744): the raw-moment scheme of
+ * Eq. LBErawmomentcuboidlattice,
+ *   m = S P f,  m~ = m + B^-1 {Lambda (B m^eq - B m) + (I - Lambda/2) B Phi},  f~ = P^-1 S^-1 m~,
+ * with m^eq from Eq. 10, Phi from Eq. 11, the same B grouping and relaxation
+ * rates as App D and "the same corrections via the extended moment equilibria"
+ * (P:L744): the second-order diagonal equilibria carry the theta terms of
+ * P:L1171-1178, and the strain rates come from the raw non-equilibrium moments
+ * n^(1) through the same C/R system. */
+void oracle_collide_raw(const oracle_ctx *c, const double *f, double *ft) {
+  const oracle_params *p = &c->p;
+  const double cs2 = p->cs2, r2 = p->r * p->r, s2 = p->s * p->s;
+  const double wn = p->omega_nu, wx = p->omega_xi, w1 = p->omega_1, wh = p->omega_high;
+  double rho, u[3];
+  oracle_hydro(&c->e[0][0], f, p->force, &rho, u);
+  const double ux = u[0], uy = u[1], uz = u[2];
+  double m[NQ], meq[NQ], phi[NQ], mt[NQ];
+  matvec(c->Q, f, m); /* m = Q f = S P f (Eq. 56, 58) */
+  oracle_raw_equilibria(rho, u, cs2, meq);
+  oracle_raw_source(u, p->force, phi);
+#define M(a, b, c_) m[midx(a, b, c_)]
+#define E(a, b, c_) meq[midx(a, b, c_)]
+#define PH(a, b, c_) phi[midx(a, b, c_)]
+#define MT(a, b, c_) mt[midx(a, b, c_)]
+  /* B: combine, for m, m^eq and Phi alike */
+  double k2s = M(2, 0, 0) + M(0, 2, 0) + M(0, 0, 2), e2s = E(2, 0, 0) + E(0, 2, 0) + E(0, 0, 2);
+  double k2d1 = M(2, 0, 0) - M(0, 2, 0), e2d1 = E(2, 0, 0) - E(0, 2, 0);
+  double k2d2 = M(2, 0, 0) - M(0, 0, 2), e2d2 = E(2, 0, 0) - E(0, 0, 2);
+  double p2s = PH(2, 0, 0) + PH(0, 2, 0) + PH(0, 0, 2), p2d1 = PH(2, 0, 0) - PH(0, 2, 0),
+         p2d2 = PH(2, 0, 0) - PH(0, 0, 2);
+  if (p->corrections != CORR_OFF) {
+    const double g = (p->corrections == CORR_FULL_LOCAL) ? 1.0 : 0.0;
+    const double an = 1.0 / wn - 0.5, ab = 1.0 / wx - 0.5;
+    double th_sx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * an;
+    double th_bx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * ab;
+    double th_sy = -rho * (g * 3.0 * uy * uy + 3.0 * cs2 - r2) * an;
+    double th_by = -rho * (g * 3.0 * uy * uy + 3.0 * cs2 - r2) * ab;
+    double th_sz = -rho * (g * 3.0 * uz * uz + 3.0 * cs2 - s2) * an;
+    double th_bz = -rho * (g * 3.0 * uz * uz + 3.0 * cs2 - s2) * ab;
+    /* raw non-equilibrium moments n^(1), e_rho = 0 (reading R1) */
+    double Rb = k2s - e2s, Rs1 = k2d1 - e2d1, Rs2 = k2d2 - e2d2;
+    double Csx = (-2.0 * cs2 / wn + (3.0 * cs2 - 1.0) / 2.0 + g * 3.0 * ux * ux / 2.0) * rho;
+    double Cbx = (-2.0 * cs2 / wx + (3.0 * cs2 - 1.0) / 2.0 + g * 3.0 * ux * ux / 2.0) * rho;
+    double Csy = (2.0 * cs2 / wn - (3.0 * cs2 - r2) / 2.0 - g * 3.0 * uy * uy / 2.0) * rho;
+    double Cby = (-2.0 * cs2 / wx + (3.0 * cs2 - r2) / 2.0 + g * 3.0 * uy * uy / 2.0) * rho;
+    double Csz = (2.0 * cs2 / wn - (3.0 * cs2 - s2) / 2.0 - g * 3.0 * uz * uz / 2.0) * rho;
+    double Cbz = (-2.0 * cs2 / wx + (3.0 * cs2 - s2) / 2.0 + g * 3.0 * uz * uz / 2.0) * rho;
+    double dxux = (-Csz * Cby * Rs1 - Csy * (Cbz * Rs2 - Csz * Rb)) /
+                  (-Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx));
+    double dyuy = (Rs1 - Csx * dxux) / Csy;
+    double dzuz = (Rs2 - Csx * dxux) / Csz;
+    e2s += th_bx * dxux + th_by * dyuy + th_bz * dzuz;
+    e2d1 += th_sx * dxux - th_sy * dyuy;
+    e2d2 += th_sx * dxux - th_sz * dzuz;
+  }
+  double k3s1 = M(1, 2, 0) + M(1, 0, 2), k3m1 = M(1, 2, 0) - M(1, 0, 2);
+  double k3s2 = M(2, 1, 0) + M(0, 1, 2), k3m2 = M(2, 1, 0) - M(0, 1, 2);
+  double k3s3 = M(2, 0, 1) + M(0, 2, 1), k3m3 = M(2, 0, 1) - M(0, 2, 1);
+  double e3s1 = E(1, 2, 0) + E(1, 0, 2), e3m1 = E(1, 2, 0) - E(1, 0, 2);
+  double e3s2 = E(2, 1, 0) + E(0, 1, 2), e3m2 = E(2, 1, 0) - E(0, 1, 2);
+  double e3s3 = E(2, 0, 1) + E(0, 2, 1), e3m3 = E(2, 0, 1) - E(0, 2, 1);
+  double k4s = M(2, 2, 0) + M(2, 0, 2) + M(0, 2, 2), e4s = E(2, 2, 0) + E(2, 0, 2) + E(0, 2, 2);
+  double k4d1 = M(2, 2, 0) + M(2, 0, 2) - M(0, 2, 2), e4d1 = E(2, 2, 0) + E(2, 0, 2) - E(0, 2, 2);
+  double k4d2 = M(2, 2, 0) - M(2, 0, 2), e4d2 = E(2, 2, 0) - E(2, 0, 2);
+  /* relaxation with sources (Phi is zero from third order on) */
+  MT(0, 0, 0) = M(0, 0, 0);
+  MT(1, 0, 0) = M(1, 0, 0) + w1 * (E(1, 0, 0) - M(1, 0, 0)) + (1.0 - w1 / 2.0) * PH(1, 0, 0);
+  MT(0, 1, 0) = M(0, 1, 0) + w1 * (E(0, 1, 0) - M(0, 1, 0)) + (1.0 - w1 / 2.0) * PH(0, 1, 0);
+  MT(0, 0, 1) = M(0, 0, 1) + w1 * (E(0, 0, 1) - M(0, 0, 1)) + (1.0 - w1 / 2.0) * PH(0, 0, 1);
+  MT(1, 1, 0) = M(1, 1, 0) + wn * (E(1, 1, 0) - M(1, 1, 0)) + (1.0 - wn / 2.0) * PH(1, 1, 0);
+  MT(1, 0, 1) = M(1, 0, 1) + wn * (E(1, 0, 1) - M(1, 0, 1)) + (1.0 - wn / 2.0) * PH(1, 0, 1);
+  MT(0, 1, 1) = M(0, 1, 1) + wn * (E(0, 1, 1) - M(0, 1, 1)) + (1.0 - wn / 2.0) * PH(0, 1, 1);
+  double k2st = k2s + wx * (e2s - k2s) + (1.0 - wx / 2.0) * p2s;
+  double k2d1t = k2d1 + wn * (e2d1 - k2d1) + (1.0 - wn / 2.0) * p2d1;
+  double k2d2t = k2d2 + wn * (e2d2 - k2d2) + (1.0 - wn / 2.0) * p2d2;
+  double k3s1t = k3s1 + wh * (e3s1 - k3s1), k3m1t = k3m1 + wh * (e3m1 - k3m1);
+  double k3s2t = k3s2 + wh * (e3s2 - k3s2), k3m2t = k3m2 + wh * (e3m2 - k3m2);
+  double k3s3t = k3s3 + wh * (e3s3 - k3s3), k3m3t = k3m3 + wh * (e3m3 - k3m3);
+  MT(1, 1, 1) = M(1, 1, 1) + wh * (E(1, 1, 1) - M(1, 1, 1));
+  MT(2, 1, 1) = M(2, 1, 1) + wh * (E(2, 1, 1) - M(2, 1, 1));
+  MT(1, 2, 1) = M(1, 2, 1) + wh * (E(1, 2, 1) - M(1, 2, 1));
+  MT(1, 1, 2) = M(1, 1, 2) + wh * (E(1, 1, 2) - M(1, 1, 2));
+  double k4st = k4s + wh * (e4s - k4s), k4d1t = k4d1 + wh * (e4d1 - k4d1), k4d2t = k4d2 + wh * (e4d2 - k4d2);
+  MT(1, 2, 2) = M(1, 2, 2) + wh * (E(1, 2, 2) - M(1, 2, 2));
+  MT(2, 1, 2) = M(2, 1, 2) + wh * (E(2, 1, 2) - M(2, 1, 2));
+  MT(2, 2, 1) = M(2, 2, 1) + wh * (E(2, 2, 1) - M(2, 2, 1));
+  MT(2, 2, 2) = M(2, 2, 2) + wh * (E(2, 2, 2) - M(2, 2, 2));
+  /* B^-1 */
+  MT(2, 0, 0) = (k2st + k2d1t + k2d2t) / 3.0;
+  MT(0, 2, 0) = (k2st - 2.0 * k2d1t + k2d2t) / 3.0;
+  MT(0, 0, 2) = (k2st + k2d1t - 2.0 * k2d2t) / 3.0;
+  MT(1, 2, 0) = (k3s1t + k3m1t) / 2.0;
+  MT(1, 0, 2) = (k3s1t - k3m1t) / 2.0;
+  MT(2, 1, 0) = (k3s2t + k3m2t) / 2.0;
+  MT(0, 1, 2) = (k3s2t - k3m2t) / 2.0;
+  MT(2, 0, 1) = (k3s3t + k3m3t) / 2.0;
+  MT(0, 2, 1) = (k3s3t - k3m3t) / 2.0;
+  MT(2, 2, 0) = (k4st + k4d1t + 2.0 * k4d2t) / 4.0;
+  MT(2, 0, 2) = (k4st + k4d1t - 2.0 * k4d2t) / 4.0;
+  MT(0, 2, 2) = (k4st - k4d1t) / 2.0;
+#undef M
+#undef E
+#undef PH
+#undef MT
+  matvec(c->Qinv, mt, ft); /* f~ = Q^-1 m~ = P^-1 S^-1 m~ */
+}
+
 /* ------------------------------------------------------------- boundaries */
 
 /* Momentum-augmented halfway bounce-back term for the incoming direction q at
@@ -460,7 +582,10 @@ void oracle_step(const oracle_ctx *c, const double *fsrc, double *fdst) {
     for (int y = 0; y < p->ny; ++y)
       for (int x = 0; x < p->nx; ++x) {
         for (int q = 0; q < NQ; ++q) f[q] = pull(c, fsrc, x, y, z, q);
-        oracle_collide(c, f, ft);
+        if (p->model == 1)
+          oracle_collide_raw(c, f, ft);
+        else
+          oracle_collide(c, f, ft);
         int64_t i = nid(p, x, y, z);
         for (int q = 0; q < NQ; ++q) fdst[(int64_t)q * nn + i] = ft[q];
       }

@@ -25,6 +25,8 @@ BC_PERIODIC, BC_BOUNCE_BACK, BC_MOVING_WALL, BC_FREE_SLIP = 0, 1, 2, 3
 CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF = 0, 1, 2
 # storage precision
 PREC_FP64, PREC_FP32 = 0, 1
+# collision model
+MODEL_CM, MODEL_RM = 0, 1
 
 
 def auto_cs2(r: float, s: float) -> float:
@@ -65,6 +67,7 @@ class Workload:
     init: str = "rest"          # 'rest' | 'tgv' | 'shear_layer' | 'random'
     u0: float = 0.0
     seed: int = 2107
+    model: int = 0              # 0: 3DCCM (central moments), 1: 3DCRM (raw moments)
 
     @property
     def cs2_value(self) -> float:
@@ -92,7 +95,7 @@ class Workload:
                     cs2=self.cs2_value, omega_nu=self.omega_nu, omega_xi=self.omega_xi,
                     omega_1=self.omega_1, omega_high=self.omega_high,
                     force=tuple(self.force), bc=tuple(self.bc), wall_u=self.wall_u,
-                    corrections=self.corrections, precision=self.precision)
+                    corrections=self.corrections, precision=self.precision, model=self.model)
 
 
 P = BC_PERIODIC

@@ -27,12 +27,17 @@ def _decay_rate(o, proj, n_skip, n_meas):
 
 
 def _tgv2d_rate(plane, r, s, nphys, nu, corr, amp=1e-4):
+    return _tgv2d_rate_model(plane, r, s, nphys, nu, corr, amp, model=0)
+
+
+def _tgv2d_rate_model(plane, r, s, nphys, nu, corr, amp=1e-4, model=0):
     """Exact z-invariant 2D TGV in `plane` with equal physical wavelength nphys
     along both axes; amplitude decays as exp(-2 nu k^2 t)."""
     cs2 = synth.auto_cs2(r, s)
     sp = {"x": 1.0, "y": r, "z": s}
     n = {d: (int(round(nphys / sp[d])) if d in plane else 1) for d in "xyz"}
-    o = O.Oracle(n["x"], n["y"], n["z"], r, s, cs2, synth.omega_from_nu(nu, cs2), corrections=corr)
+    o = O.Oracle(n["x"], n["y"], n["z"], r, s, cs2, synth.omega_from_nu(nu, cs2), corrections=corr,
+                 model=model)
     k = 2 * np.pi / nphys
     Z, Y, X = np.meshgrid(np.arange(n["z"]) * s, np.arange(n["y"]) * r, np.arange(n["x"]) * 1.0,
                           indexing="ij")
