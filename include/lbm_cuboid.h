@@ -71,6 +71,12 @@ typedef enum {
   LBM_FP32_STORAGE = 1 /* fp32 populations in HBM, fp64 arithmetic in registers */
 } lbm_prec;
 
+/* Collision model. */
+typedef enum {
+  LBM_MODEL_CM = 0, /* 3DCCM-LBM: central moments (Eq. LBEcentralmomentcuboidlattice) */
+  LBM_MODEL_RM = 1  /* 3DCRM-LBM: raw moments, same corrections (P:L642-648, L744(ii), L1011) */
+} lbm_model;
+
 typedef enum {
   LBM_HALO_AUTO = 0, /* 1 GPU + periodic z: wrap inside the kernel; else NCCL ghost planes */
   LBM_HALO_NCCL = 1  /* always exchange ghost planes with NCCL (also world == 1: send to self) */
@@ -93,6 +99,10 @@ typedef struct {
                                   [rank*nz/world, (rank+1)*nz/world) */
   int32_t device;              /* CUDA device ordinal of this rank */
   int32_t halo;                /* lbm_halo */
+  int32_t graphs;              /* CUDA graphs for step(n): 0 auto (replay captured 32-step graphs when
+                                  the slab has < 4M nodes and no ghost exchange), 1 never, 2 always
+                                  (when no ghost exchange) */
+  int32_t model;               /* lbm_model */
   const void *nccl_uid;        /* 128-byte ncclUniqueId from lbm_cuboid_nccl_unique_id() on rank 0,
                                   broadcast by the caller; required iff NCCL ghost exchange is used */
   void *stream;                /* cudaStream_t for all compute work; NULL -> library-owned stream */

@@ -490,6 +490,136 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, 
   }
 }
 
+// ------------------------------------------------ 3DCRM raw-moment kernel
+// The raw-moment variant of P:L642-648 (Eq. LBErawmomentcuboidlattice), named
+// 3DCRM at P:L1011: the same pipeline without F / F^-1; raw moments relax to the
+// Eq. 10 equilibria (which factorise per axis: rho E_x[i] E_y[j] E_z[k] with
+// E = (1, u, cs2 + u^2)) with the Eq. 11 sources (zero from third order on), the
+// same B grouping, rates and theta corrections; strain rates from the raw
+// non-equilibrium moments.
+
+// scale raw moments by the axis speed (App B): (m0, m1, m2) -> (m0, c m1, c^2 m2)
+template <int AX>
+__device__ __forceinline__ void scale_pass(double (&f)[27], double c, double c2) {
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int q = a * Axis<AX>::o1 + b * Axis<AX>::o2;
+      f[q + Axis<AX>::st] *= c;
+      f[q + 2 * Axis<AX>::st] *= c2;
+    }
+}
+
+// per-axis inverse with u = 0 (App F + App G): f0 = k0 - k2/c^2, f+- = (k2/c^2 +- k1/c)/2
+template <int AX>
+__device__ __forceinline__ void unscale_inverse_pass(double (&f)[27], double h1, double h2) {
+#pragma unroll
+  for (int b = 0; b < 3; ++b)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int q = a * Axis<AX>::o1 + b * Axis<AX>::o2;
+      const double k0 = f[q], t1 = f[q + Axis<AX>::st] * h1, t2 = f[q + 2 * Axis<AX>::st] * h2;
+      f[q] = t2 - t1;
+      f[q + Axis<AX>::st] = fma(-2.0, t2, k0);
+      f[q + 2 * Axis<AX>::st] = t2 + t1;
+    }
+}
+
+__device__ __forceinline__ void collide_raw(const Consts& c, double (&f)[27], double rho, double inv_rho,
+                                            double ux, double uy, double uz) {
+#define M(i, j, k) f[LBM_Q(i, j, k)]
+  const double w1 = c.w1, wn = c.wn, wh = c.wh;
+  const double Ex[3] = {1.0, ux, c.cs2 + ux * ux}, Ey[3] = {1.0, uy, c.cs2 + uy * uy},
+               Ez[3] = {1.0, uz, c.cs2 + uz * uz};
+  const double Fx = c.F[0], Fy = c.F[1], Fz = c.F[2];
+  // first order: m + w1 (rho u - m) + (1 - w1/2) F
+  M(1, 0, 0) = fma(w1, rho * ux - M(1, 0, 0), M(1, 0, 0)) + (1.0 - 0.5 * w1) * Fx;
+  M(0, 1, 0) = fma(w1, rho * uy - M(0, 1, 0), M(0, 1, 0)) + (1.0 - 0.5 * w1) * Fy;
+  M(0, 0, 1) = fma(w1, rho * uz - M(0, 0, 1), M(0, 0, 1)) + (1.0 - 0.5 * w1) * Fz;
+  // off-diagonal second order, sources F_a u_b + F_b u_a
+  const double hn = 1.0 - 0.5 * wn;
+  M(1, 1, 0) = fma(wn, rho * ux * uy - M(1, 1, 0), M(1, 1, 0)) + hn * (Fx * uy + Fy * ux);
+  M(1, 0, 1) = fma(wn, rho * ux * uz - M(1, 0, 1), M(1, 0, 1)) + hn * (Fx * uz + Fz * ux);
+  M(0, 1, 1) = fma(wn, rho * uy * uz - M(0, 1, 1), M(0, 1, 1)) + hn * (Fy * uz + Fz * uy);
+  // diagonal second order (B, corrections, relax, B^-1)
+  {
+    const double k200 = M(2, 0, 0), k020 = M(0, 2, 0), k002 = M(0, 0, 2);
+    const double k2s = k200 + k020 + k002, k2d1 = k200 - k020, k2d2 = k200 - k002;
+    const double q200 = rho * Ex[2], q020 = rho * Ey[2], q002 = rho * Ez[2];
+    double e2s = q200 + q020 + q002, e2d1 = q200 - q020, e2d2 = q200 - q002;
+    if (c.corr_on) {
+      const double ga = 1.5 * c.galias;
+      const double qx = ga * ux * ux, qy = ga * uy * uy, qz = ga * uz * uz;
+      const double Csx = -c.csn + 0.5 * c.gx + qx;
+      const double Cbx = -c.csx + 0.5 * c.gx + qx;
+      const double Csy = c.csn - 0.5 * c.gy - qy;
+      const double Cby = -c.csx + 0.5 * c.gy + qy;
+      const double Csz = c.csn - 0.5 * c.gz - qz;
+      const double Cbz = -c.csx + 0.5 * c.gz + qz;
+      const double Rb = (k2s - e2s) * inv_rho, Rs1 = (k2d1 - e2d1) * inv_rho, Rs2 = (k2d2 - e2d2) * inv_rho;
+      const double t1 = Csx * Cbz - Csz * Cbx;
+      const double inv_det = 1.0 / (-Csx * Csz * Cby - Csy * t1);
+      const double dxux = (-Csz * Cby * Rs1 - Csy * (Cbz * Rs2 - Csz * Rb)) * inv_det;
+      const double dyuy = (Csx * (Rs2 * Cbz - Csz * Rb) - Rs1 * t1) * inv_det;
+      const double dzuz = (Csx * Cby * (Rs1 - Rs2) - Csy * (Csx * Rb - Rs2 * Cbx)) * inv_det;
+      const double tx = (2.0 * qx + c.gx) * dxux, ty = (2.0 * qy + c.gy) * dyuy, tz = (2.0 * qz + c.gz) * dzuz;
+      const double rn = rho * c.an, rb = rho * c.ab;
+      e2d1 -= rn * (tx - ty);
+      e2d2 -= rn * (tx - tz);
+      e2s -= rb * (tx + ty + tz);
+    }
+    const double p2s = 2.0 * (Fx * ux + Fy * uy + Fz * uz), p2d1 = 2.0 * (Fx * ux - Fy * uy),
+                 p2d2 = 2.0 * (Fx * ux - Fz * uz);
+    const double s2s = fma(c.wx, e2s - k2s, k2s) + (1.0 - 0.5 * c.wx) * p2s;
+    const double s2d1 = fma(wn, e2d1 - k2d1, k2d1) + hn * p2d1;
+    const double s2d2 = fma(wn, e2d2 - k2d2, k2d2) + hn * p2d2;
+    const double third = 1.0 / 3.0;
+    M(2, 0, 0) = (s2s + s2d1 + s2d2) * third;
+    M(0, 2, 0) = (s2s - 2.0 * s2d1 + s2d2) * third;
+    M(0, 0, 2) = (s2s + s2d1 - 2.0 * s2d2) * third;
+  }
+  // third and higher orders: one rate per B group -> per moment, toward Eq. 10
+  const double om = 1.0 - wh, wr = wh * rho;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+        if (i + j + k >= 3) M(i, j, k) = fma(om, M(i, j, k), wr * Ex[i] * Ey[j] * Ez[k]);
+#undef M
+}
+
+template <typename T>
+__global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T* __restrict__ dst,
+                                                   const __grid_constant__ Consts c, int zbeg, int zstride) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int y = idx / c.nx;
+  const int x = idx - y * c.nx;
+  const int z = zbeg + blockIdx.y * zstride;
+  double f[27];
+  gather<T>(src, c, x, y, z, f);
+  raw_pass<0>(f);
+  raw_pass<1>(f);
+  raw_pass<2>(f);
+  const double rho = f[LBM_Q(0, 0, 0)];
+  const double inv_rho = 1.0 / rho;
+  const double ux = (f[LBM_Q(1, 0, 0)] + 0.5 * c.F[0]) * inv_rho;
+  const double uy = fma(c.r, f[LBM_Q(0, 1, 0)], 0.5 * c.F[1]) * inv_rho;
+  const double uz = fma(c.s, f[LBM_Q(0, 0, 1)], 0.5 * c.F[2]) * inv_rho;
+  scale_pass<1>(f, c.r, c.r2);
+  scale_pass<2>(f, c.s, c.s2);
+  collide_raw(c, f, rho, inv_rho, ux, uy, uz);
+  unscale_inverse_pass<2>(f, c.h1z, c.h2z);
+  unscale_inverse_pass<1>(f, c.h1y, c.h2y);
+  unscale_inverse_pass<0>(f, 0.5, 0.5);
+  T* out = dst + (long long)(z + 1) * c.plane + idx;
+#pragma unroll
+  for (int q = 0; q < 27; ++q) stcs<T>(out + q * c.nxy, f[q]);
+}
+
 // -------------------------------------------------------------- init kernel
 // f~ = f^eq(rho, u + F/(2 rho)) (reading R8).  The raw equilibria of Eq. 10
 // factorise per axis into 1D Maxwellian moments (1, u, cs2 + u^2), so

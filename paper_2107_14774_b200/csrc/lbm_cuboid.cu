@@ -56,6 +56,8 @@ int fail(int code, const char* fmt, ...) {
 
 constexpr size_t kStageBytes = size_t(256) << 20;  // host<->device staging chunk
 constexpr size_t kMaxTimedLaunches = 1 << 16;
+constexpr int kGraphSteps = 32;                 // steps per captured graph (even: ends on the same buffer)
+constexpr int64_t kGraphMaxNodes = 4 << 20;     // auto mode: graphs below this many local nodes
 
 }  // namespace
 
@@ -80,6 +82,9 @@ struct lbm_cuboid {
   size_t stage_bytes = 0;
   double* d_check = nullptr;
   int64_t launches = 0, cs_launches = 0, steps = 0;
+  // CUDA graphs of kGraphSteps steps, one per starting buffer
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  bool capturing = false;
   // optional per-launch timing of the collide-stream kernel (lbm_cuboid_timing)
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_t;
@@ -118,6 +123,8 @@ int validate(const lbm_cuboid_params* p) {
   if (p->corrections < 0 || p->corrections > 2) return fail(LBM_EINVAL, "corrections must be an lbm_corr");
   if (p->precision < 0 || p->precision > 1) return fail(LBM_EINVAL, "precision must be an lbm_prec");
   if (p->halo < 0 || p->halo > 1) return fail(LBM_EINVAL, "halo must be an lbm_halo");
+  if (p->graphs < 0 || p->graphs > 2) return fail(LBM_EINVAL, "graphs must be 0, 1 or 2");
+  if (p->model < 0 || p->model > 1) return fail(LBM_EINVAL, "model must be an lbm_model");
   for (int d = 0; d < 3; ++d)
     if (!std::isfinite(p->force[d])) return fail(LBM_EINVAL, "force must be finite");
   if (!std::isfinite(p->wall_u)) return fail(LBM_EINVAL, "wall_u must be finite");
@@ -207,7 +214,14 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
     h->ev_t.push_back({a, b});
     CU(cudaEventRecord(a, s));
   }
-  if (h->paper_rates) {
+  if (h->p.model == LBM_MODEL_RM) {
+    if (fp64)
+      lbm::k_collide_stream_raw<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg,
+                                                                  zstride);
+    else
+      lbm::k_collide_stream_raw<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg,
+                                                                 zstride);
+  } else if (h->paper_rates) {
     if (fp64)
       lbm::k_collide_stream_paper<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg,
                                                                     zstride);
@@ -225,8 +239,49 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
     CU(cudaEventRecord(h->ev_t.back().second, s));
     h->ev_t_nodes.push_back(int64_t(nplanes) * h->nxy);
   }
-  h->launches++;
-  h->cs_launches++;
+  if (!h->capturing) {
+    h->launches++;
+    h->cs_launches++;
+  }
+  return LBM_OK;
+}
+
+void drop_graphs(lbm_cuboid* h) {
+  for (auto& g : h->gexec)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+}
+
+bool use_graphs(const lbm_cuboid* h) {
+  if (h->ghost || h->timing || h->p.graphs == 1) return false;
+  return h->p.graphs == 2 || h->nxy * h->nzl < kGraphMaxNodes;
+}
+
+// capture kGraphSteps single-GPU steps starting from buffer `start`
+int capture_graph(lbm_cuboid* h, int start) {
+  cudaGraph_t g = nullptr;
+  CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  h->capturing = true;
+  int rc = LBM_OK, c = start;
+  for (int t = 0; t < kGraphSteps && rc == LBM_OK; ++t) {
+    rc = launch_cs(h, h->buf[c], h->buf[c ^ 1], 0, h->nzl, 1, h->stream);
+    c ^= 1;
+  }
+  h->capturing = false;
+  cudaError_t e = cudaStreamEndCapture(h->stream, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  if (e != cudaSuccess) return fail(LBM_ECUDA, "cudaStreamEndCapture: %s", cudaGetErrorString(e));
+  e = cudaGraphInstantiate(&h->gexec[start], g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    h->gexec[start] = nullptr;
+    return fail(LBM_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+  }
   return LBM_OK;
 }
 
@@ -488,6 +543,16 @@ int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
   if (nsteps < 0) return fail(LBM_EINVAL, "nsteps must be >= 0");
   int rc = set_device(h);
   if (rc) return rc;
+  if (use_graphs(h)) {
+    while (nsteps >= kGraphSteps) {
+      if (!h->gexec[h->cur] && (rc = capture_graph(h, h->cur))) return rc;
+      CU(cudaGraphLaunch(h->gexec[h->cur], h->stream));
+      h->launches += kGraphSteps;
+      h->cs_launches += kGraphSteps;
+      h->steps += kGraphSteps;
+      nsteps -= kGraphSteps;  // kGraphSteps is even: h->cur is unchanged
+    }
+  }
   for (int64_t t = 0; t < nsteps; ++t) {
     void* src = h->buf[h->cur];
     void* dst = h->buf[h->cur ^ 1];
@@ -628,6 +693,7 @@ int lbm_cuboid_set_force(lbm_cuboid_t* h, const double force[3]) {
     h->p.force[d] = force[d];
     h->c.F[d] = force[d];
   }
+  drop_graphs(h);  // the parameter block is baked into captured launches
   return LBM_OK;
 }
 
@@ -640,7 +706,7 @@ int lbm_cuboid_info(const lbm_cuboid_t* h, int64_t out[8]) {
   out[4] = h->nxy * h->nzl;
   out[5] = h->buf_elems * int64_t(h->elem);
   out[6] = h->ghost ? 1 : 0;
-  out[7] = h->paper_rates ? 1 : 0;
+  out[7] = (h->paper_rates && h->p.model == LBM_MODEL_CM) ? 1 : 0;
   return LBM_OK;
 }
 
@@ -699,6 +765,7 @@ int lbm_cuboid_destroy(lbm_cuboid_t* h) {
   if (h->stage) cudaFree(h->stage);
   if (h->d_check) cudaFree(h->d_check);
   clear_timing(h);
+  drop_graphs(h);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
   return LBM_OK;

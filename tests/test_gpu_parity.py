@@ -277,3 +277,50 @@ def test_full_size_bench_config_sampled(P, precision):
             assert (np.abs(got - ref) / np.abs(ref)).max() <= TOL32
     d = g.check()
     assert d["bad_nodes"] == 0
+
+
+# ------------------------------------------------------------ 3DCRM (raw moments)
+@pytest.mark.parametrize("name", ["tgv_full", "cavity100", "shear", "duct"])
+def test_parity_raw_model_fp64(P, name):
+    w = CASES[name].scaled(model=synth.MODEL_RM)
+    o, g = _init_both(P, w, seed=31)
+    o.step(100)
+    g.step(100)
+    _cmp(o, g)
+
+
+def test_parity_raw_model_generic_rates_fp32(P):
+    w = synth.Workload("rm-generic", 17, 11, 9, r=0.5, s=1.0, nu=0.02, omega_xi=0.7, omega_1=1.3,
+                       omega_high=1.1, force=(1e-5, 2e-5, -1e-5), init="random", seed=8, model=synth.MODEL_RM)
+    o, g = _init_both(P, w, seed=8, noneq=1e-3)
+    o.step(60)
+    g.step(60)
+    _cmp(o, g)
+    w32 = w.scaled(precision=synth.PREC_FP32)
+    o, g = _init_both(P, w32, seed=8)
+    o.step(60)
+    g.step(60)
+    _cmp(o, g, prec=1)
+
+
+# ------------------------------------------------------------------- CUDA graphs
+@pytest.mark.parametrize("model", [0, 1])
+def test_graphs_bitwise_equal_to_stream_launches(P, model):
+    """step(n) replays captured 32-step graphs on small grids (graphs=0 auto);
+    the result is bitwise the one of plain launches (graphs=1)."""
+    w = CASES["tgv_full"].scaled(model=model)
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 41)
+    a = _gpu(P, w, graphs=1)
+    b = _gpu(P, w, graphs=0)
+    a.init_fields(rho, u)
+    b.init_fields(rho, u)
+    for n in (100, 7, 64):  # 3 graphs + 4 launches, 7 launches, 2 graphs
+        a.step(n)
+        b.step(n)
+    assert a.info()["steps"] == b.info()["steps"] == 171
+    assert np.array_equal(a.get_populations(), b.get_populations())
+    b.set_force((1e-5, 0.0, 0.0))  # invalidates the captured graphs
+    a.set_force((1e-5, 0.0, 0.0))
+    a.step(40)
+    b.step(40)
+    assert np.array_equal(a.get_populations(), b.get_populations())
