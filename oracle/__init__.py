@@ -51,6 +51,7 @@ def lib():
         L.oracle_create.restype = ctypes.c_void_p
         L.oracle_create.argtypes = [ctypes.POINTER(_Params)]
         L.oracle_destroy.argtypes = [ctypes.c_void_p]
+        L.oracle_set_force.argtypes = [ctypes.c_void_p, _D]
         L.oracle_ctx_Qinv.restype = _D
         L.oracle_ctx_Qinv.argtypes = [ctypes.c_void_p]
         L.oracle_velocities.argtypes = [ctypes.c_double, ctypes.c_double, _D]
@@ -204,6 +205,10 @@ class Oracle:
         fn = lib().oracle_collide_raw if self.model == 1 else lib().oracle_collide
         fn(self._ctx, _p(_arr(f, 27)), _p(out))
         return out
+
+    def set_force(self, F):
+        self.force = _arr(F, 3).copy()
+        lib().oracle_set_force(self._ctx, _p(self.force))
 
     def lid_term(self, q, rho_f):
         return lib().oracle_lid_term(self._ctx, int(q), float(rho_f))

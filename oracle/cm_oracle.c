@@ -265,6 +265,11 @@ oracle_ctx *oracle_create(const oracle_params *p) {
 
 void oracle_destroy(oracle_ctx *c) { free(c); }
 
+/* Replace the body force (time-periodic forcing F = F_m cos(omega t)). */
+void oracle_set_force(oracle_ctx *c, const double *F) {
+  for (int d = 0; d < 3; ++d) c->p.force[d] = F[d];
+}
+
 const double *oracle_ctx_Qinv(const oracle_ctx *c) { return c->Qinv; }
 
 /* f^eq = Q^-1 m^eq with m^eq from Eq. 10 (the procedure stated at P:L759). */

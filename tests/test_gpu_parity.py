@@ -324,3 +324,20 @@ def test_graphs_bitwise_equal_to_stream_launches(P, model):
     a.step(40)
     b.step(40)
     assert np.array_equal(a.get_populations(), b.get_populations())
+
+
+def test_parity_time_periodic_force(P):
+    """Per-step force updates (F = F_m cos(omega t)) through
+    lbm_cuboid_set_force on both sides, walls in y and z."""
+    w = synth.CONFIGS["duct"].scaled(nx=4, ny=22, nz=11, force=(0.0, 0.0, 0.0))
+    o, g = _init_both(P, w, seed=43)
+    for n in range(1, 61):
+        F = (1e-4 * np.cos(2 * np.pi * n / 40), 0.0, 2e-5 * np.sin(2 * np.pi * n / 40))
+        o.set_force(F)
+        g.set_force(F)
+        o.step(1)
+        g.step(1)
+    _cmp(o, g)
+    ro, uo = o.macroscopic()
+    rg, ug = g.get_macroscopic()
+    assert np.abs(ro - rg).max() < 1e-12 and np.abs(uo - ug).max() < 1e-12

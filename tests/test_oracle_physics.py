@@ -181,3 +181,32 @@ def test_periodic_momentum_grows_by_force():
     o.step(10)
     p1 = np.einsum("qzyx,qd->d", o.f, e)
     assert np.allclose(p1 - p0, 10 * w.nodes * np.array(w.force), rtol=1e-9, atol=1e-14)
+
+
+def test_pulsatile_duct_womersley():
+    """Time-periodic forcing F_x = F_m cos(omega t) in a square duct (PAPER.md
+    L804-853) against the Womersley series (erratum E14 form, studies/analytic.py):
+    Wo = 3.09, 2a = 16 on a (r, s) = (0.5, 1) lattice, second period, four phases,
+    L2 error < 2%."""
+    from studies.analytic import womersley
+
+    r, s, ny, nz, twoa, T, Wo = 0.5, 1.0, 32, 16, 16.0, 1600, 3.09
+    a = twoa / 2
+    om = 2 * np.pi / T
+    nu = a * a * om / Wo ** 2
+    Fm = 1e-5
+    cs2 = synth.auto_cs2(r, s)
+    o = O.Oracle(1, ny, nz, r, s, cs2, synth.omega_from_nu(nu, cs2), bc=(0, 0, 1, 1, 1, 1))
+    o.init_fields(np.ones((nz, ny, 1)), np.zeros((3, nz, ny, 1)))
+    y = (np.arange(ny) + 0.5) * r - a
+    z = (np.arange(nz) + 0.5) * s - a
+    Z, Y = np.meshgrid(z, y, indexing="ij")
+    errs = []
+    for n in range(1, 2 * T + 1):
+        o.set_force((Fm * np.cos(om * n), 0.0, 0.0))
+        o.step(1)
+        if n > T and (2 * T - n) % (T // 4) == 0:
+            u = o.macroscopic()[1][0][:, :, 0]
+            ua = womersley(Y, Z, n, a, Fm, om, nu)
+            errs.append(np.sqrt(((u - ua) ** 2).sum() / (ua ** 2).sum()))
+    assert len(errs) == 4 and max(errs) < 0.02, errs
