@@ -47,6 +47,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nz-per-gpu", type=int, default=None, help="override the per-GPU slab depth")
+    ap.add_argument("--halo", choices=["auto", "nccl"], default="auto",
+                    help="nccl: force the multi-GPU step structure (boundary launch, NCCL ghost-plane "
+                         "exchange on the comm stream, interior launch) even on one GPU (send to self)")
     return ap.parse_args()
 
 
@@ -215,6 +218,8 @@ def run_cuda(args):
     kw = w.params()
     if world > 1:
         lat = P.distributed_lattice(device=local, **kw)
+    elif args.halo == "nccl":
+        lat = P.Lattice(device=local, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id(), **kw)
     else:
         lat = P.Lattice(device=local, **kw)
     stream = lat.stream
@@ -231,13 +236,17 @@ def run_cuda(args):
         torch.cuda.synchronize(local)
 
     def barrier():
+        # drain this rank's GPU work (incl. the library's NCCL halo stream) before
+        # the torch collective, so two communicators never have interleaved work in flight
+        torch.cuda.synchronize(local)
         if world > 1:
             dist.barrier(device_ids=[local])
-        torch.cuda.synchronize(local)
+            torch.cuda.synchronize(local)
 
     def max_over_ranks(x):
         if world == 1:
             return x
+        torch.cuda.synchronize(local)
         t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
@@ -335,7 +344,8 @@ def run_cuda(args):
             "config": {"workload": w.name, "grid_global": [w.nx, w.ny, w.nz], "nodes_global": w.nodes,
                        "r": w.r, "s": w.s, "nu": w.nu, "corrections": "FULL_LOCAL", "storage": prec,
                        "l2": "working set per step (58 GB/GPU fp64) >> 126 MB L2; no flush needed",
-                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
+                       "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "halo": "nccl ghost planes" if lat.info()["nccl_halo"] else "in-kernel wrap"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "bad_nodes": bad}
     print(json.dumps(line), flush=True)

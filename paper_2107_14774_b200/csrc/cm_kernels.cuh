@@ -61,7 +61,22 @@ struct Consts {
   double c4, c6;              // cs2^2, cs2^3
   double lid_u;               // moving-wall speed U
   double lid_c[3];            // Eq. 69 coefficient per e_z in {-1,0,1}: cs2/(2 r^2) * phi_z(e_z)
+  long long buf_elems;        // elements of one population buffer (bounds checks)
+  unsigned int* dbg_flag;     // LBM_DEBUG_BOUNDS builds: set to 1 on an out-of-range access
 };
+
+// Debug builds (-DLBM_DEBUG_BOUNDS): every population access of the collide-stream
+// kernels is checked against the buffer; a violation sets *dbg_flag and is skipped.
+#ifdef LBM_DEBUG_BOUNDS
+#define LBM_CHECK_LD(base, p, c)                                                          \
+  (((unsigned long long)((p) - (base)) < (unsigned long long)(c).buf_elems)              \
+       ? (p)                                                                              \
+       : (atomicOr((c).dbg_flag, 1u), (base)))
+#define LBM_CHECK_ST(base, p, c) LBM_CHECK_LD(base, p, c)
+#else
+#define LBM_CHECK_LD(base, p, c) (p)
+#define LBM_CHECK_ST(base, p, c) (p)
+#endif
 
 // ------------------------------------------------------------------ memory ops
 template <typename T> __device__ __forceinline__ double ldg(const T* p);
@@ -273,7 +288,7 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           const int q = LBM_Q(i, j, k);
-          f[q] = ldg(pz[k] + q * c.nxy + sy[j] + sx[i]);
+          f[q] = ldg(LBM_CHECK_LD(src, pz[k] + q * c.nxy + sy[j] + sx[i], c));
         }
     return;
   }
@@ -288,7 +303,7 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
   double rho_f = 0.0;  // reading R4: rho_f = sum_b f~_b(x_f, t) at the wall-adjacent node
   if (cym == FK_MOVING) {
 #pragma unroll
-    for (int q = 0; q < 27; ++q) rho_f += ldg(p0 + q * c.nxy + own);
+    for (int q = 0; q < 27; ++q) rho_f += ldg(LBM_CHECK_LD(src, p0 + q * c.nxy + own, c));
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k)
@@ -305,7 +320,7 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
                             (kz == FK_BOUNCE || kz == FK_MOVING);
         if (noslip) {
           // halfway bounce-back from the own node's opposite direction
-          double v = ldg(p0 + LBM_Q(2 - i, 2 - j, 2 - k) * c.nxy + own);
+          double v = ldg(LBM_CHECK_LD(src, p0 + LBM_Q(2 - i, 2 - j, 2 - k) * c.nxy + own, c));
           if (ky == FK_MOVING)  // Eq. 69: + rho_f U e_x cs2/(2 r^2) phi_z(e_z)
             v = fma(rho_f * c.lid_u * (double)ex, c.lid_c[k], v);
           f[q] = v;
@@ -317,7 +332,7 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
           const int xs = mx ? x : sx[i];
           const int ys = my ? y * nx : sy[j];
           const T* zs = mz ? p0 : pz[k];
-          f[q] = ldg(zs + LBM_Q(qi, qj, qk) * c.nxy + ys + xs);
+          f[q] = ldg(LBM_CHECK_LD(src, zs + LBM_Q(qi, qj, qk) * c.nxy + ys + xs, c));
         }
       }
 }
@@ -365,7 +380,7 @@ __global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __r
 
   T* out = dst + (long long)(z + 1) * c.plane + idx;
 #pragma unroll
-  for (int q = 0; q < 27; ++q) stcs<T>(out + q * c.nxy, f[q]);
+  for (int q = 0; q < 27; ++q) stcs<T>(LBM_CHECK_ST(dst, out + q * c.nxy, c), f[q]);
 }
 
 // ------------------------------------- paper-rate kernel (omega_1 = omega_high = 1)
@@ -483,9 +498,9 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, 
     for (int j = 0; j < 3; ++j) {
       double fm, f0, fp;
       inv1d<true, true>(H0[j], H1[j], H2[j], ux, 0.5, 0.5, fm, f0, fp);
-      stcs<T>(out + LBM_Q(0, j, k) * c.nxy, fm);
-      stcs<T>(out + LBM_Q(1, j, k) * c.nxy, f0);
-      stcs<T>(out + LBM_Q(2, j, k) * c.nxy, fp);
+      stcs<T>(LBM_CHECK_ST(dst, out + LBM_Q(0, j, k) * c.nxy, c), fm);
+      stcs<T>(LBM_CHECK_ST(dst, out + LBM_Q(1, j, k) * c.nxy, c), f0);
+      stcs<T>(LBM_CHECK_ST(dst, out + LBM_Q(2, j, k) * c.nxy, c), fp);
     }
   }
 }
@@ -617,7 +632,7 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T*
   unscale_inverse_pass<0>(f, 0.5, 0.5);
   T* out = dst + (long long)(z + 1) * c.plane + idx;
 #pragma unroll
-  for (int q = 0; q < 27; ++q) stcs<T>(out + q * c.nxy, f[q]);
+  for (int q = 0; q < 27; ++q) stcs<T>(LBM_CHECK_ST(dst, out + q * c.nxy, c), f[q]);
 }
 
 // -------------------------------------------------------------- init kernel

@@ -81,6 +81,7 @@ struct lbm_cuboid {
   double* stage = nullptr;
   size_t stage_bytes = 0;
   double* d_check = nullptr;
+  unsigned int* d_dbg = nullptr;  // bounds-check flag (written only by LBM_DEBUG_BOUNDS builds)
   int64_t launches = 0, cs_launches = 0, steps = 0;
   // CUDA graphs of kGraphSteps steps, one per starting buffer
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -193,6 +194,7 @@ void fill_consts(lbm_cuboid* h) {
     c.face[4] = kind(p.bc[4]);
     c.face[5] = kind(p.bc[5]);
   }
+  c.buf_elems = h->buf_elems;
   c.has_walls = 0;
   for (int f = 0; f < 6; ++f)
     if (c.face[f] >= lbm::FK_BOUNCE && c.face[f] <= lbm::FK_SLIP) c.has_walls = 1;
@@ -489,6 +491,10 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
     if (cudaMemsetAsync(h->buf[i], 0, bytes, h->stream) != cudaSuccess)
       return bail(fail(LBM_ECUDA, "cudaMemsetAsync failed"));
   if (cudaMalloc(&h->d_check, 8 * sizeof(double)) != cudaSuccess) return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
+  if (cudaMalloc(&h->d_dbg, sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemsetAsync(h->d_dbg, 0, sizeof(unsigned int), h->stream) != cudaSuccess)
+    return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
+  h->c.dbg_flag = h->d_dbg;
   if (h->ghost) {
     if (!p->nccl_uid) return bail(fail(LBM_EINVAL, "nccl_uid is required for the NCCL ghost exchange"));
     if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
@@ -580,6 +586,11 @@ int lbm_cuboid_sync(lbm_cuboid_t* h) {
   if ((rc = wait_halo(h))) return rc;
   CU(cudaStreamSynchronize(h->stream));
   if (h->comm_stream) CU(cudaStreamSynchronize(h->comm_stream));
+#ifdef LBM_DEBUG_BOUNDS
+  unsigned int flag = 0;
+  CU(cudaMemcpy(&flag, h->d_dbg, sizeof(flag), cudaMemcpyDeviceToHost));
+  if (flag) return fail(LBM_ECUDA, "bounds check: a collide-stream kernel accessed outside its buffer");
+#endif
   return LBM_OK;
 }
 
@@ -764,6 +775,7 @@ int lbm_cuboid_destroy(lbm_cuboid_t* h) {
       if (h->buf[i]) cudaFree(h->buf[i]);
   if (h->stage) cudaFree(h->stage);
   if (h->d_check) cudaFree(h->d_check);
+  if (h->d_dbg) cudaFree(h->d_dbg);
   clear_timing(h);
   drop_graphs(h);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

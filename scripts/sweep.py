@@ -27,6 +27,7 @@ VARIANTS = {
     "b256m3": ["LBM_BLOCK=256", "LBM_MINB=3"],
     "ld1": ["LBM_LDMODE=1"],
     "st1": ["LBM_STMODE=1"],
+    "debug": ["LBM_DEBUG_BOUNDS=1"],
 }
 
 
