@@ -66,6 +66,9 @@ def lib():
         L.oracle_feq.argtypes = [ctypes.c_void_p, ctypes.c_double, _D, _D]
         L.oracle_collide.argtypes = [ctypes.c_void_p, _D, _D]
         L.oracle_collide_raw.argtypes = [ctypes.c_void_p, _D, _D]
+        L.oracle_collide_g.argtypes = [ctypes.c_void_p, _D, _D, _D]
+        L.oracle_collide_raw_g.argtypes = [ctypes.c_void_p, _D, _D, _D]
+        L.oracle_density_gradient.argtypes = [ctypes.c_void_p, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, _D]
         L.oracle_raw_source.argtypes = [_D, _D, _D]
         L.oracle_lid_term.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_double]
         L.oracle_lid_term.restype = ctypes.c_double
@@ -200,11 +203,20 @@ class Oracle:
         lib().oracle_feq(self._ctx, float(rho), _p(_arr(u, 3)), _p(out))
         return out
 
-    def collide(self, f):
+    def collide(self, f, grad_rho=None):
         out = np.zeros(27)
-        fn = lib().oracle_collide_raw if self.model == 1 else lib().oracle_collide
-        fn(self._ctx, _p(_arr(f, 27)), _p(out))
+        if grad_rho is None:
+            fn = lib().oracle_collide_raw if self.model == 1 else lib().oracle_collide
+            fn(self._ctx, _p(_arr(f, 27)), _p(out))
+        else:
+            fn = lib().oracle_collide_raw_g if self.model == 1 else lib().oracle_collide_g
+            fn(self._ctx, _p(_arr(f, 27)), _p(_arr(grad_rho, 3)), _p(out))
         return out
+
+    def density_gradient(self, rho, x, y, z):
+        g = np.zeros(3)
+        lib().oracle_density_gradient(self._ctx, _p(_arr(rho, self.f[0].size)), int(x), int(y), int(z), _p(g))
+        return g
 
     def set_force(self, F):
         self.force = _arr(F, 3).copy()

@@ -66,7 +66,7 @@ static const int MIDX[3][3][3] = {
 #define midx(m, n, p) MIDX[m][n][p]
 
 enum { BC_PERIODIC = 0, BC_BOUNCE_BACK = 1, BC_MOVING_WALL = 2, BC_FREE_SLIP = 3 };
-enum { CORR_FULL_LOCAL = 0, CORR_LOW_MACH = 1, CORR_OFF = 2 };
+enum { CORR_FULL_LOCAL = 0, CORR_LOW_MACH = 1, CORR_OFF = 2, CORR_FULL_FD = 3 };
 
 typedef struct {
   int32_t nx, ny, nz;
@@ -283,7 +283,13 @@ void oracle_feq(const oracle_ctx *c, double rho, const double *u, double *feq) {
 
 /* One node: f (pre-collision, time t) -> f~ (post-collision), following the
  * step list of P:L687-729 with App D for the relaxation. */
-void oracle_collide(const oracle_ctx *c, const double *f, double *ft) {
+void oracle_collide_g(const oracle_ctx *c, const double *f, const double *grad_rho, double *ft);
+void oracle_collide_raw_g(const oracle_ctx *c, const double *f, const double *grad_rho, double *ft);
+
+void oracle_collide(const oracle_ctx *c, const double *f, double *ft) { oracle_collide_g(c, f, NULL, ft); }
+
+/* grad_rho: density gradient at the node for CORR_FULL_FD (NULL: zero). */
+void oracle_collide_g(const oracle_ctx *c, const double *f, const double *grad_rho, double *ft) {
   const oracle_params *p = &c->p;
   const double cs2 = p->cs2, r2 = p->r * p->r, s2 = p->s * p->s;
   const double wn = p->omega_nu, wx = p->omega_xi, w1 = p->omega_1, wh = p->omega_high;
@@ -311,7 +317,7 @@ void oracle_collide(const oracle_ctx *c, const double *f, double *ft) {
    * with the coefficients of P:L1171-1180 and local strain rates of P:L1183-1203. */
   double k2s_eq = 3.0 * cs2 * rho, k2d1_eq = 0.0, k2d2_eq = 0.0;
   if (p->corrections != CORR_OFF) {
-    const double g = (p->corrections == CORR_FULL_LOCAL) ? 1.0 : 0.0; /* aliasing (3u^2) terms */
+    const double g = (p->corrections == CORR_FULL_LOCAL || p->corrections == CORR_FULL_FD) ? 1.0 : 0.0; /* aliasing (3u^2) terms */
     const double an = 1.0 / wn - 0.5, ab = 1.0 / wx - 0.5;
     double th_sx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * an;
     double th_bx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * ab;
@@ -319,8 +325,20 @@ void oracle_collide(const oracle_ctx *c, const double *f, double *ft) {
     double th_by = -rho * (g * 3.0 * uy * uy + 3.0 * cs2 - r2) * ab;
     double th_sz = -rho * (g * 3.0 * uz * uz + 3.0 * cs2 - s2) * an;
     double th_bz = -rho * (g * 3.0 * uz * uz + 3.0 * cs2 - s2) * ab;
-    /* e_sr1 = e_sr2 = e_br = 0 (reading R1: lambda terms off) */
-    double Rb = k2s - 3.0 * cs2 * rho, Rs1 = k2d1, Rs2 = k2d2;
+    /* density-gradient terms: only in CORR_FULL_FD
+     * (reading R1: FULL_LOCAL and LOW_MACH set lambda = e_rho = 0) */
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    if (p->corrections == CORR_FULL_FD && grad_rho) {
+      gx = grad_rho[0];
+      gy = grad_rho[1];
+      gz = grad_rho[2];
+    }
+    double lam_sx = -(3.0 * cs2 - 1.0) * an * ux, lam_bx = -(3.0 * cs2 - 1.0) * ab * ux;
+    double lam_sy = +(3.0 * cs2 - r2) * an * uy, lam_by = -(3.0 * cs2 - r2) * ab * uy;
+    double lam_sz = +(3.0 * cs2 - s2) * an * uz, lam_bz = -(3.0 * cs2 - s2) * ab * uz;
+    double A = 0.5 * (3.0 * cs2 - 1.0) * ux, B = 0.5 * (3.0 * cs2 - r2) * uy, C = 0.5 * (3.0 * cs2 - s2) * uz;
+    double e_sr1 = -A * gx + B * gy, e_sr2 = -A * gx + C * gz, e_br = -A * gx - B * gy - C * gz;
+    double Rb = k2s - 3.0 * cs2 * rho + e_br, Rs1 = k2d1 + e_sr1, Rs2 = k2d2 + e_sr2;
     double Csx = (-2.0 * cs2 / wn + (3.0 * cs2 - 1.0) / 2.0 + g * 3.0 * ux * ux / 2.0) * rho;
     double Cbx = (-2.0 * cs2 / wx + (3.0 * cs2 - 1.0) / 2.0 + g * 3.0 * ux * ux / 2.0) * rho;
     double Csy = (2.0 * cs2 / wn - (3.0 * cs2 - r2) / 2.0 - g * 3.0 * uy * uy / 2.0) * rho;
@@ -331,9 +349,9 @@ void oracle_collide(const oracle_ctx *c, const double *f, double *ft) {
                   (-Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx));
     double dyuy = (Rs1 - Csx * dxux) / Csy;
     double dzuz = (Rs2 - Csx * dxux) / Csz;
-    k2s_eq = 3.0 * cs2 * rho + (th_bx * dxux + th_by * dyuy + th_bz * dzuz);
-    k2d1_eq = th_sx * dxux - th_sy * dyuy;
-    k2d2_eq = th_sx * dxux - th_sz * dzuz;
+    k2s_eq = 3.0 * cs2 * rho + (th_bx * dxux + th_by * dyuy + th_bz * dzuz + lam_bx * gx + lam_by * gy + lam_bz * gz);
+    k2d1_eq = th_sx * dxux - th_sy * dyuy + lam_sx * gx + lam_sy * gy;
+    k2d2_eq = th_sx * dxux - th_sz * dzuz + lam_sx * gx + lam_sz * gz;
   }
   /* higher-order equilibria, Eq. 64 */
   const double c4r = cs2 * cs2 * rho, c6r = cs2 * cs2 * cs2 * rho;
@@ -410,7 +428,9 @@ void oracle_raw_source(const double *u, const double *F, double *phi) {
  * (P:L744): the second-order diagonal equilibria carry the theta terms of
  * P:L1171-1178, and the strain rates come from the raw non-equilibrium moments
  * n^(1) through the same C/R system. */
-void oracle_collide_raw(const oracle_ctx *c, const double *f, double *ft) {
+void oracle_collide_raw(const oracle_ctx *c, const double *f, double *ft) { oracle_collide_raw_g(c, f, NULL, ft); }
+
+void oracle_collide_raw_g(const oracle_ctx *c, const double *f, const double *grad_rho, double *ft) {
   const oracle_params *p = &c->p;
   const double cs2 = p->cs2, r2 = p->r * p->r, s2 = p->s * p->s;
   const double wn = p->omega_nu, wx = p->omega_xi, w1 = p->omega_1, wh = p->omega_high;
@@ -432,7 +452,7 @@ void oracle_collide_raw(const oracle_ctx *c, const double *f, double *ft) {
   double p2s = PH(2, 0, 0) + PH(0, 2, 0) + PH(0, 0, 2), p2d1 = PH(2, 0, 0) - PH(0, 2, 0),
          p2d2 = PH(2, 0, 0) - PH(0, 0, 2);
   if (p->corrections != CORR_OFF) {
-    const double g = (p->corrections == CORR_FULL_LOCAL) ? 1.0 : 0.0;
+    const double g = (p->corrections == CORR_FULL_LOCAL || p->corrections == CORR_FULL_FD) ? 1.0 : 0.0;
     const double an = 1.0 / wn - 0.5, ab = 1.0 / wx - 0.5;
     double th_sx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * an;
     double th_bx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * ab;
@@ -440,8 +460,19 @@ void oracle_collide_raw(const oracle_ctx *c, const double *f, double *ft) {
     double th_by = -rho * (g * 3.0 * uy * uy + 3.0 * cs2 - r2) * ab;
     double th_sz = -rho * (g * 3.0 * uz * uz + 3.0 * cs2 - s2) * an;
     double th_bz = -rho * (g * 3.0 * uz * uz + 3.0 * cs2 - s2) * ab;
-    /* raw non-equilibrium moments n^(1), e_rho = 0 (reading R1) */
-    double Rb = k2s - e2s, Rs1 = k2d1 - e2d1, Rs2 = k2d2 - e2d2;
+    double gx = 0.0, gy = 0.0, gz = 0.0;
+    if (p->corrections == CORR_FULL_FD && grad_rho) {
+      gx = grad_rho[0];
+      gy = grad_rho[1];
+      gz = grad_rho[2];
+    }
+    double lam_sx = -(3.0 * cs2 - 1.0) * an * ux, lam_bx = -(3.0 * cs2 - 1.0) * ab * ux;
+    double lam_sy = +(3.0 * cs2 - r2) * an * uy, lam_by = -(3.0 * cs2 - r2) * ab * uy;
+    double lam_sz = +(3.0 * cs2 - s2) * an * uz, lam_bz = -(3.0 * cs2 - s2) * ab * uz;
+    double A = 0.5 * (3.0 * cs2 - 1.0) * ux, B = 0.5 * (3.0 * cs2 - r2) * uy, C = 0.5 * (3.0 * cs2 - s2) * uz;
+    /* raw non-equilibrium moments n^(1) plus e_rho */
+    double Rb = k2s - e2s + (-A * gx - B * gy - C * gz), Rs1 = k2d1 - e2d1 + (-A * gx + B * gy),
+           Rs2 = k2d2 - e2d2 + (-A * gx + C * gz);
     double Csx = (-2.0 * cs2 / wn + (3.0 * cs2 - 1.0) / 2.0 + g * 3.0 * ux * ux / 2.0) * rho;
     double Cbx = (-2.0 * cs2 / wx + (3.0 * cs2 - 1.0) / 2.0 + g * 3.0 * ux * ux / 2.0) * rho;
     double Csy = (2.0 * cs2 / wn - (3.0 * cs2 - r2) / 2.0 - g * 3.0 * uy * uy / 2.0) * rho;
@@ -452,9 +483,9 @@ void oracle_collide_raw(const oracle_ctx *c, const double *f, double *ft) {
                   (-Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx));
     double dyuy = (Rs1 - Csx * dxux) / Csy;
     double dzuz = (Rs2 - Csx * dxux) / Csz;
-    e2s += th_bx * dxux + th_by * dyuy + th_bz * dzuz;
-    e2d1 += th_sx * dxux - th_sy * dyuy;
-    e2d2 += th_sx * dxux - th_sz * dzuz;
+    e2s += th_bx * dxux + th_by * dyuy + th_bz * dzuz + lam_bx * gx + lam_by * gy + lam_bz * gz;
+    e2d1 += th_sx * dxux - th_sy * dyuy + lam_sx * gx + lam_sy * gy;
+    e2d2 += th_sx * dxux - th_sz * dzuz + lam_sx * gx + lam_sz * gz;
   }
   double k3s1 = M(1, 2, 0) + M(1, 0, 2), k3m1 = M(1, 2, 0) - M(1, 0, 2);
   double k3s2 = M(2, 1, 0) + M(0, 1, 2), k3m2 = M(2, 1, 0) - M(0, 1, 2);
@@ -578,22 +609,66 @@ static double pull(const oracle_ctx *c, const double *fs, int x, int y, int z, i
   return fs[(int64_t)qs * nn + nid(p, src[0], src[1], src[2])];
 }
 
-/* One time step on the whole grid: fdst = collide(pull(fsrc)). */
+/* Isotropic second-order density gradient (reading R16):
+ *   d_d rho(x) = (1/cs2) sum_a w_a e_ad rho(x + e_a),
+ * w_a the cuboid rest weights (f^eq at rho = 1, u = 0), which satisfy
+ * sum_a w_a e_a e_a = cs2 I.  A neighbour across a wall takes rho of the node
+ * itself (zero normal gradient); periodic faces wrap. */
+void oracle_density_gradient(const oracle_ctx *c, const double *rho, int x, int y, int z, double *g) {
+  const oracle_params *p = &c->p;
+  double w[NQ], u0[3] = {0.0, 0.0, 0.0};
+  oracle_feq(c, 1.0, u0, w);
+  int n[3] = {p->nx, p->ny, p->nz}, xyz[3] = {x, y, z};
+  g[0] = g[1] = g[2] = 0.0;
+  for (int a = 0; a < NQ; ++a) {
+    int e[3] = {EX[a], EY[a], EZ[a]}, nb[3];
+    int wall = 0;
+    for (int d = 0; d < 3; ++d) {
+      nb[d] = xyz[d] + e[d];
+      if (nb[d] < 0 || nb[d] >= n[d]) {
+        int face = (nb[d] < 0) ? 2 * d : 2 * d + 1;
+        if (p->bc[face] != BC_PERIODIC) wall = 1;
+        nb[d] = wrap(nb[d], n[d]);
+      }
+    }
+    double rn = wall ? rho[nid(p, x, y, z)] : rho[nid(p, nb[0], nb[1], nb[2])];
+    for (int d = 0; d < 3; ++d) g[d] += w[a] * c->e[a][d] * rn;
+  }
+  for (int d = 0; d < 3; ++d) g[d] /= p->cs2;
+}
+
+/* One time step on the whole grid: fdst = collide(pull(fsrc)).  With
+ * CORR_FULL_FD the step is done in two passes: pull every node and form the
+ * same-time density field, then collide with its isotropic gradient. */
 void oracle_step(const oracle_ctx *c, const double *fsrc, double *fdst) {
   const oracle_params *p = &c->p;
   const int64_t nn = (int64_t)p->nx * p->ny * p->nz;
-  double f[NQ], ft[NQ];
+  double f[NQ], ft[NQ], g[3];
+  const int fd = (p->corrections == CORR_FULL_FD);
+  double *rho = NULL;
+  if (fd) {
+    rho = (double *)malloc(sizeof(double) * nn);
+    for (int z = 0; z < p->nz; ++z)
+      for (int y = 0; y < p->ny; ++y)
+        for (int x = 0; x < p->nx; ++x) {
+          double r0 = 0.0;
+          for (int q = 0; q < NQ; ++q) r0 += pull(c, fsrc, x, y, z, q);
+          rho[nid(p, x, y, z)] = r0;
+        }
+  }
   for (int z = 0; z < p->nz; ++z)
     for (int y = 0; y < p->ny; ++y)
       for (int x = 0; x < p->nx; ++x) {
         for (int q = 0; q < NQ; ++q) f[q] = pull(c, fsrc, x, y, z, q);
+        if (fd) oracle_density_gradient(c, rho, x, y, z, g);
         if (p->model == 1)
-          oracle_collide_raw(c, f, ft);
+          oracle_collide_raw_g(c, f, fd ? g : NULL, ft);
         else
-          oracle_collide(c, f, ft);
+          oracle_collide_g(c, f, fd ? g : NULL, ft);
         int64_t i = nid(p, x, y, z);
         for (int q = 0; q < NQ; ++q) fdst[(int64_t)q * nn + i] = ft[q];
       }
+  free(rho);
 }
 
 /* n steps, ping-ponging between f and tmp; result ends in f. */
