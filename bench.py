@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nz-per-gpu", type=int, default=None, help="override the per-GPU slab depth")
+    ap.add_argument("--corrections", choices=["full_local", "low_mach", "off", "full_fd"], default="full_local")
+    ap.add_argument("--model", choices=["cm", "rm"], default="cm")
     ap.add_argument("--halo", choices=["auto", "nccl"], default="auto",
                     help="nccl: force the multi-GPU step structure (boundary launch, NCCL ghost-plane "
                          "exchange on the comm stream, interior launch) even on one GPU (send to self)")
@@ -57,6 +59,9 @@ def workload(args, world):
     w = synth.CONFIGS[args.workload]
     if args.precision == "fp32":
         w = w.scaled(precision=synth.PREC_FP32)
+    corr = {"full_local": synth.CORR_FULL_LOCAL, "low_mach": synth.CORR_LOW_MACH, "off": synth.CORR_OFF,
+            "full_fd": synth.CORR_FULL_FD}[args.corrections]
+    w = w.scaled(corrections=corr, model=synth.MODEL_RM if args.model == "rm" else synth.MODEL_CM)
     nzl = args.nz_per_gpu or w.nz
     if args.workload == "weak":
         w = w.scaled(nz=nzl * world)      # weak scaling: fixed 512^3 per GPU
@@ -323,7 +328,8 @@ def run_cuda(args):
     achieved = bpn * nodes_per_launch / (kernel_ms * 1e-3) / 1e9
     prec = "fp64" if w.precision == 0 else "fp32"
     traffic = ncu_traffic(w.name, prec)
-    kname = "k_collide_stream_paper" if lat.info()["paper_rate_kernel"] else "k_collide_stream"
+    kname = ("k_collide_stream_raw" if w.model == synth.MODEL_RM else
+             "k_collide_stream_paper" if lat.info()["paper_rate_kernel"] else "k_collide_stream")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src,
             "kernel": f"{kname}<{'double' if prec == 'fp64' else 'float'}>",
@@ -342,7 +348,8 @@ def run_cuda(args):
             "scaling": "weak" if args.workload == "weak" else "strong", "vs_baseline": None,
             "dtype": "f64" if prec == "fp64" else "f64-arith/f32-storage", "data": "synthetic",
             "config": {"workload": w.name, "grid_global": [w.nx, w.ny, w.nz], "nodes_global": w.nodes,
-                       "r": w.r, "s": w.s, "nu": w.nu, "corrections": "FULL_LOCAL", "storage": prec,
+                       "r": w.r, "s": w.s, "nu": w.nu, "corrections": args.corrections.upper(),
+                       "model": "3DCCM" if w.model == 0 else "3DCRM", "storage": prec,
                        "l2": "working set per step (58 GB/GPU fp64) >> 126 MB L2; no flush needed",
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                        "halo": "nccl ghost planes" if lat.info()["nccl_halo"] else "in-kernel wrap"},

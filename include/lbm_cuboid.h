@@ -63,7 +63,10 @@ typedef enum {
 typedef enum {
   LBM_CORR_FULL_LOCAL = 0, /* theta with the 3u^2 aliasing terms; local strain rates; lambda = e_rho = 0 */
   LBM_CORR_LOW_MACH = 1,   /* 3u^2 terms dropped (in theta and in the strain-rate solve) */
-  LBM_CORR_OFF = 2         /* no corrections (ablation) */
+  LBM_CORR_OFF = 2,        /* no corrections (ablation) */
+  LBM_CORR_FULL_FD = 3     /* FULL_LOCAL plus the density-gradient terms lambda and e_rho,
+                              with the isotropic lattice gradient of a same-time density field:
+                              one extra density pass per step (+216 B/node of HBM traffic) */
 } lbm_corr;
 
 typedef enum {

@@ -61,6 +61,7 @@ struct Consts {
   double c4, c6;              // cs2^2, cs2^3
   double lid_u;               // moving-wall speed U
   double lid_c[3];            // Eq. 69 coefficient per e_z in {-1,0,1}: cs2/(2 r^2) * phi_z(e_z)
+  double phx[3], phy[3], phz[3];  // cuboid rest weights per axis: phi(0) = 1 - cs2/c^2, phi(+-1) = cs2/(2c^2)
   long long buf_elems;        // elements of one population buffer (bounds checks)
   unsigned int* dbg_flag;     // LBM_DEBUG_BOUNDS builds: set to 1 on an out-of-range access
 };
@@ -173,10 +174,12 @@ __device__ __forceinline__ void inverse_pass(double (&f)[27], double u, double h
 // App D on the central moments held in slots K(i,j,k) = f[i+3j+9k].
 // Local strain rates are solved with Cramer's rule on the
 // system divided by rho (one reciprocal); lambda = e_rho = 0 (reading R1).
+template <bool FD = false>
 __device__ __forceinline__ void second_order_diag(const Consts& c, double rho, double inv_rho,
                                                   double ux, double uy, double uz,
                                                   double k200, double k020, double k002,
-                                                  double& o200, double& o020, double& o002) {
+                                                  double& o200, double& o020, double& o002,
+                                                  double gxr = 0.0, double gyr = 0.0, double gzr = 0.0) {
   const double k2s = k200 + k020 + k002;  // B
   const double k2d1 = k200 - k020;
   const double k2d2 = k200 - k002;
@@ -192,8 +195,17 @@ __device__ __forceinline__ void second_order_diag(const Consts& c, double rho, d
     const double Cby = -c.csx + 0.5 * c.gy + qy;
     const double Csz = c.csn - 0.5 * c.gz - qz;
     const double Cbz = -c.csx + 0.5 * c.gz + qz;
-    // R / rho with e_rho = 0
-    const double Rb = (k2s - c3r) * inv_rho, Rs1 = k2d1 * inv_rho, Rs2 = k2d2 * inv_rho;
+    // R / rho; e_rho terms only with FD (reading R1)
+    double Rb = (k2s - c3r) * inv_rho, Rs1 = k2d1 * inv_rho, Rs2 = k2d2 * inv_rho;
+    double lsx = 0.0, lsy = 0.0, lsz = 0.0;  // A d_x rho, B d_y rho, C d_z rho
+    if (FD) {
+      lsx = 0.5 * c.gx * ux * gxr;
+      lsy = 0.5 * c.gy * uy * gyr;
+      lsz = 0.5 * c.gz * uz * gzr;
+      Rb += (-lsx - lsy - lsz) * inv_rho;
+      Rs1 += (-lsx + lsy) * inv_rho;
+      Rs2 += (-lsx + lsz) * inv_rho;
+    }
     const double t1 = Csx * Cbz - Csz * Cbx;
     const double det = -Csx * Csz * Cby - Csy * t1;
     const double inv_det = 1.0 / det;
@@ -208,6 +220,12 @@ __device__ __forceinline__ void second_order_diag(const Consts& c, double rho, d
     e2d1 = -rn * (tx - ty);          // Eq. 63
     e2d2 = -rn * (tx - tz);          // Eq. 63
     e2s = c3r - rb * (tx + ty + tz); // Eq. 63
+    if (FD) {
+      // lambda_s x = -2 a_n A, lambda_s y = +2 a_n B, ..., times the gradients
+      e2d1 += 2.0 * c.an * (-lsx + lsy);
+      e2d2 += 2.0 * c.an * (-lsx + lsz);
+      e2s += 2.0 * c.ab * (-lsx - lsy - lsz);
+    }
   }
   const double s2s = fma(c.wx, e2s - k2s, k2s);
   const double s2d1 = fma(c.wn, e2d1 - k2d1, k2d1);
@@ -219,8 +237,10 @@ __device__ __forceinline__ void second_order_diag(const Consts& c, double rho, d
 }
 
 // Generic relaxation (any omega_1, omega_high): all 27 central moments are in f.
+template <bool FD>
 __device__ __forceinline__ void collide_generic(const Consts& c, double (&f)[27], double rho,
-                                                double inv_rho, double ux, double uy, double uz) {
+                                                double inv_rho, double ux, double uy, double uz,
+                                                double gxr, double gyr, double gzr) {
 #define K(i, j, k) f[LBM_Q(i, j, k)]
   const double w1 = c.w1, wn = c.wn, wh = c.wh;
   // first order: k~ = k + w1 (0 - k) + (1 - w1/2) F
@@ -232,7 +252,8 @@ __device__ __forceinline__ void collide_generic(const Consts& c, double (&f)[27]
   K(1, 0, 1) *= (1.0 - wn);
   K(0, 1, 1) *= (1.0 - wn);
   double o200, o020, o002;
-  second_order_diag(c, rho, inv_rho, ux, uy, uz, K(2, 0, 0), K(0, 2, 0), K(0, 0, 2), o200, o020, o002);
+  second_order_diag<FD>(c, rho, inv_rho, ux, uy, uz, K(2, 0, 0), K(0, 2, 0), K(0, 0, 2), o200, o020, o002, gxr,
+                        gyr, gzr);
   K(2, 0, 0) = o200;
   K(0, 2, 0) = o020;
   K(0, 0, 2) = o002;
@@ -337,6 +358,62 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
       }
 }
 
+// ----------------------------------------------- isotropic density gradient
+// d_d rho = (1/cs2) sum_a w_a e_ad rho(x + e_a) (reading R16)
+// with the cuboid rest weights w_a = phi_x phi_y phi_z; per axis this is a central
+// difference 1/(2c) weighted by the rest weights of the two other axes.  A
+// neighbour across a wall face takes the node's own density.  rf has the
+// population-buffer plane structure: rf[(z_local + 1) * nxy + y * nx + x].
+__device__ __forceinline__ void density_gradient(const double* __restrict__ rf, const Consts& c, int x, int y,
+                                                 int z, double& gx, double& gy, double& gz) {
+  const int nx = c.nx;
+  auto is_wall = [](int fk) { return fk >= FK_BOUNCE && fk <= FK_SLIP; };
+  const int xs[3] = {(x == 0) ? nx - 1 : x - 1, x, (x == nx - 1) ? 0 : x + 1};
+  const bool cx[3] = {x == 0 && is_wall(c.face[0]), false, x == nx - 1 && is_wall(c.face[1])};
+  const int ys[3] = {((y == 0) ? c.ny - 1 : y - 1) * nx, y * nx, ((y == c.ny - 1) ? 0 : y + 1) * nx};
+  const bool cy[3] = {y == 0 && is_wall(c.face[2]), false, y == c.ny - 1 && is_wall(c.face[3])};
+  int zm = z - 1, zp = z + 1;
+  if (z == 0 && c.face[4] == FK_WRAP) zm = c.nzl - 1;
+  if (z == c.nzl - 1 && c.face[5] == FK_WRAP) zp = 0;
+  const long long zb[3] = {(long long)(zm + 1) * c.nxy, (long long)(z + 1) * c.nxy, (long long)(zp + 1) * c.nxy};
+  const bool cz[3] = {z == 0 && is_wall(c.face[4]), false, z == c.nzl - 1 && is_wall(c.face[5])};
+  const double own = __ldg(rf + zb[1] + ys[1] + xs[1]);
+  double sx = 0.0, sy = 0.0, sz = 0.0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        if (i == 1 && j == 1 && k == 1) continue;
+        const bool wall = cx[i] || cy[j] || cz[k];
+        const double v = wall ? own : __ldg(rf + zb[k] + ys[j] + xs[i]);
+        if (i != 1) sx += (i == 2 ? 1.0 : -1.0) * c.phy[j] * c.phz[k] * v;
+        if (j != 1) sy += (j == 2 ? 1.0 : -1.0) * c.phx[i] * c.phz[k] * v;
+        if (k != 1) sz += (k == 2 ? 1.0 : -1.0) * c.phx[i] * c.phy[j] * v;
+      }
+  gx = 0.5 * sx;
+  gy = c.h1y * sy;
+  gz = c.h1z * sz;
+}
+
+// density pass for FULL_FD: rho(x, t+1) = sum_q f_q(x, t+1) of the pulled populations
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_density(const T* __restrict__ src, double* __restrict__ rho_out,
+                                                    const __grid_constant__ Consts c, int zbeg, int zstride) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int y = idx / c.nx;
+  const int x = idx - y * c.nx;
+  const int z = zbeg + blockIdx.y * zstride;
+  double f[27];
+  gather<T>(src, c, x, y, z, f);
+  double r0 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 27; ++q) r0 += f[q];
+  rho_out[(long long)(z + 1) * c.nxy + idx] = r0;
+}
+
 // --------------------------------------------------------- the fused kernel
 // One thread per node of planes zbeg + i*zstride, i < gridDim.y, of the local slab.
 #if LBM_MINB > 0
@@ -344,9 +421,10 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
 #else
 #define LBM_CS_BOUNDS __launch_bounds__(kBlock)
 #endif
-template <typename T>
+template <typename T, bool FD>
 __global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __restrict__ dst,
-                                                           const __grid_constant__ Consts c, int zbeg, int zstride) {
+                                               const double* __restrict__ rf, const __grid_constant__ Consts c,
+                                               int zbeg, int zstride) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
   const int y = idx / c.nx;
@@ -354,6 +432,9 @@ __global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __r
   const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
 
   double f[27];
+  // FULL_FD: gradient first, so its L2-resident loads overlap the population loads
+  double gxr = 0.0, gyr = 0.0, gzr = 0.0;
+  if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
   gather<T>(src, c, x, y, z, f);
 
   // m = P f (App A), per axis
@@ -371,7 +452,7 @@ __global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __r
   central_pass<1, false>(f, uy, c.r, c.r2);
   central_pass<2, false>(f, uz, c.s, c.s2);
 
-  collide_generic(c, f, rho, inv_rho, ux, uy, uz);
+  collide_generic<FD>(c, f, rho, inv_rho, ux, uy, uz, gxr, gyr, gzr);
 
   // f~ = P^-1 S^-1 F^-1 m~^c (App E, F, G), per axis
   inverse_pass<2>(f, uz, c.h1z, c.h2z);
@@ -409,9 +490,10 @@ __device__ __forceinline__ void inv1d(double k0, double k1, double k2, double u,
   fp = t2 + t1;
 }
 
-template <typename T>
+template <typename T, bool FD>
 __global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, T* __restrict__ dst,
-                                                     const __grid_constant__ Consts c, int zbeg, int zstride) {
+                                                     const double* __restrict__ rf, const __grid_constant__ Consts c,
+                                                     int zbeg, int zstride) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
   const int y = idx / c.nx;
@@ -419,6 +501,9 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, 
   const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
 
   double f[27];
+  // FULL_FD: gradient first, so its L2-resident loads overlap the population loads
+  double gxr = 0.0, gyr = 0.0, gzr = 0.0;
+  if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
   gather<T>(src, c, x, y, z, f);
 
   // raw moments up to second order, cubic units (App A restricted to m+n+p <= 2).
@@ -470,7 +555,7 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, 
 
   // collision (App D) for the second order; first order -> F/2, higher -> Eq. 64
   double K200, K020, K002;
-  second_order_diag(c, rho, inv_rho, ux, uy, uz, k200, k020, k002, K200, K020, K002);
+  second_order_diag<FD>(c, rho, inv_rho, ux, uy, uz, k200, k020, k002, K200, K020, K002, gxr, gyr, gzr);
   const double om = 1.0 - c.wn;
   const double K110 = om * k110, K101 = om * k101, K011 = om * k011;
   const double K100 = 0.5 * c.F[0], K010 = 0.5 * c.F[1], K001 = 0.5 * c.F[2];
@@ -541,8 +626,9 @@ __device__ __forceinline__ void unscale_inverse_pass(double (&f)[27], double h1,
     }
 }
 
+template <bool FD>
 __device__ __forceinline__ void collide_raw(const Consts& c, double (&f)[27], double rho, double inv_rho,
-                                            double ux, double uy, double uz) {
+                                            double ux, double uy, double uz, double gxr, double gyr, double gzr) {
 #define M(i, j, k) f[LBM_Q(i, j, k)]
   const double w1 = c.w1, wn = c.wn, wh = c.wh;
   const double Ex[3] = {1.0, ux, c.cs2 + ux * ux}, Ey[3] = {1.0, uy, c.cs2 + uy * uy},
@@ -572,7 +658,16 @@ __device__ __forceinline__ void collide_raw(const Consts& c, double (&f)[27], do
       const double Cby = -c.csx + 0.5 * c.gy + qy;
       const double Csz = c.csn - 0.5 * c.gz - qz;
       const double Cbz = -c.csx + 0.5 * c.gz + qz;
-      const double Rb = (k2s - e2s) * inv_rho, Rs1 = (k2d1 - e2d1) * inv_rho, Rs2 = (k2d2 - e2d2) * inv_rho;
+      double Rb = (k2s - e2s) * inv_rho, Rs1 = (k2d1 - e2d1) * inv_rho, Rs2 = (k2d2 - e2d2) * inv_rho;
+      double lsx = 0.0, lsy = 0.0, lsz = 0.0;  // e_rho terms, FULL_FD only
+      if (FD) {
+        lsx = 0.5 * c.gx * ux * gxr;
+        lsy = 0.5 * c.gy * uy * gyr;
+        lsz = 0.5 * c.gz * uz * gzr;
+        Rb += (-lsx - lsy - lsz) * inv_rho;
+        Rs1 += (-lsx + lsy) * inv_rho;
+        Rs2 += (-lsx + lsz) * inv_rho;
+      }
       const double t1 = Csx * Cbz - Csz * Cbx;
       const double inv_det = 1.0 / (-Csx * Csz * Cby - Csy * t1);
       const double dxux = (-Csz * Cby * Rs1 - Csy * (Cbz * Rs2 - Csz * Rb)) * inv_det;
@@ -583,6 +678,11 @@ __device__ __forceinline__ void collide_raw(const Consts& c, double (&f)[27], do
       e2d1 -= rn * (tx - ty);
       e2d2 -= rn * (tx - tz);
       e2s -= rb * (tx + ty + tz);
+      if (FD) {
+        e2d1 += 2.0 * c.an * (-lsx + lsy);
+        e2d2 += 2.0 * c.an * (-lsx + lsz);
+        e2s += 2.0 * c.ab * (-lsx - lsy - lsz);
+      }
     }
     const double p2s = 2.0 * (Fx * ux + Fy * uy + Fz * uz), p2d1 = 2.0 * (Fx * ux - Fy * uy),
                  p2d2 = 2.0 * (Fx * ux - Fz * uz);
@@ -606,15 +706,19 @@ __device__ __forceinline__ void collide_raw(const Consts& c, double (&f)[27], do
 #undef M
 }
 
-template <typename T>
+template <typename T, bool FD>
 __global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T* __restrict__ dst,
-                                                   const __grid_constant__ Consts c, int zbeg, int zstride) {
+                                                   const double* __restrict__ rf, const __grid_constant__ Consts c,
+                                                   int zbeg, int zstride) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
   const int y = idx / c.nx;
   const int x = idx - y * c.nx;
   const int z = zbeg + blockIdx.y * zstride;
   double f[27];
+  // FULL_FD: gradient first, so its L2-resident loads overlap the population loads
+  double gxr = 0.0, gyr = 0.0, gzr = 0.0;
+  if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
   gather<T>(src, c, x, y, z, f);
   raw_pass<0>(f);
   raw_pass<1>(f);
@@ -626,7 +730,7 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T*
   const double uz = fma(c.s, f[LBM_Q(0, 0, 1)], 0.5 * c.F[2]) * inv_rho;
   scale_pass<1>(f, c.r, c.r2);
   scale_pass<2>(f, c.s, c.s2);
-  collide_raw(c, f, rho, inv_rho, ux, uy, uz);
+  collide_raw<FD>(c, f, rho, inv_rho, ux, uy, uz, gxr, gyr, gzr);
   unscale_inverse_pass<2>(f, c.h1z, c.h2z);
   unscale_inverse_pass<1>(f, c.h1y, c.h2y);
   unscale_inverse_pass<0>(f, 0.5, 0.5);

@@ -75,6 +75,9 @@ struct lbm_cuboid {
   bool halo_pending = false;
   bool ghost = false;  // ghost-plane (NCCL) mode
   bool paper_rates = false;  // omega_1 = omega_high = 1 -> k_collide_stream_paper
+  bool fd = false;           // FULL_FD: density pass + isotropic gradient
+  double* d_rho = nullptr;   // FULL_FD density field, population-buffer plane structure (ghost planes)
+  cudaEvent_t ev_rho = nullptr;
   ncclComm_t comm = nullptr;
   int peer_down = -1, peer_up = -1;  // ranks owning the planes below / above, -1 none
   Consts c{};
@@ -121,7 +124,7 @@ int validate(const lbm_cuboid_params* p) {
   for (int f = 0; f < 6; ++f)
     if (p->bc[f] == LBM_BC_MOVING_WALL && f != 3)
       return fail(LBM_EINVAL, "configuration error: a moving wall is supported on the +y face only (P:L751)");
-  if (p->corrections < 0 || p->corrections > 2) return fail(LBM_EINVAL, "corrections must be an lbm_corr");
+  if (p->corrections < 0 || p->corrections > 3) return fail(LBM_EINVAL, "corrections must be an lbm_corr");
   if (p->precision < 0 || p->precision > 1) return fail(LBM_EINVAL, "precision must be an lbm_prec");
   if (p->halo < 0 || p->halo > 1) return fail(LBM_EINVAL, "halo must be an lbm_halo");
   if (p->graphs < 0 || p->graphs > 2) return fail(LBM_EINVAL, "graphs must be 0, 1 or 2");
@@ -162,7 +165,7 @@ void fill_consts(lbm_cuboid* h) {
   c.gx = 3.0 * cs2 - 1.0;
   c.gy = 3.0 * cs2 - c.r2;
   c.gz = 3.0 * cs2 - c.s2;
-  c.galias = (p.corrections == LBM_CORR_FULL_LOCAL) ? 1.0 : 0.0;
+  c.galias = (p.corrections == LBM_CORR_FULL_LOCAL || p.corrections == LBM_CORR_FULL_FD) ? 1.0 : 0.0;
   c.corr_on = (p.corrections != LBM_CORR_OFF);
   c.csn = 2.0 * cs2 / p.omega_nu;
   c.csx = 2.0 * cs2 / p.omega_xi;
@@ -195,6 +198,14 @@ void fill_consts(lbm_cuboid* h) {
     c.face[5] = kind(p.bc[5]);
   }
   c.buf_elems = h->buf_elems;
+  // rest weights of the isotropic density gradient (FULL_FD): f^eq at rho = 1, u = 0 per axis
+  const double cc[3] = {1.0, c.r2, c.s2};
+  double* ph[3] = {c.phx, c.phy, c.phz};
+  for (int d = 0; d < 3; ++d) {
+    ph[d][0] = cs2 / (2.0 * cc[d]);
+    ph[d][1] = 1.0 - cs2 / cc[d];
+    ph[d][2] = cs2 / (2.0 * cc[d]);
+  }
   c.has_walls = 0;
   for (int f = 0; f < 6; ++f)
     if (c.face[f] >= lbm::FK_BOUNCE && c.face[f] <= lbm::FK_SLIP) c.has_walls = 1;
@@ -216,26 +227,32 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
     h->ev_t.push_back({a, b});
     CU(cudaEventRecord(a, s));
   }
-  if (h->p.model == LBM_MODEL_RM) {
-    if (fp64)
-      lbm::k_collide_stream_raw<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg,
-                                                                  zstride);
-    else
-      lbm::k_collide_stream_raw<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg,
-                                                                 zstride);
-  } else if (h->paper_rates) {
-    if (fp64)
-      lbm::k_collide_stream_paper<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg,
-                                                                    zstride);
-    else
-      lbm::k_collide_stream_paper<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg,
-                                                                   zstride);
-  } else {
-    if (fp64)
-      lbm::k_collide_stream<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, h->c, zbeg, zstride);
-    else
-      lbm::k_collide_stream<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg, zstride);
-  }
+  const double* rf = h->d_rho;
+#define LBM_LAUNCH(KERNEL)                                                                                   \
+  do {                                                                                                       \
+    if (fp64) {                                                                                              \
+      if (h->fd)                                                                                             \
+        lbm::KERNEL<double, true><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, rf, h->c, zbeg, \
+                                                             zstride);                                       \
+      else                                                                                                   \
+        lbm::KERNEL<double, false><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, rf, h->c, zbeg, \
+                                                              zstride);                                      \
+    } else {                                                                                                 \
+      if (h->fd)                                                                                             \
+        lbm::KERNEL<float, true><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, rf, h->c, zbeg,    \
+                                                            zstride);                                        \
+      else                                                                                                   \
+        lbm::KERNEL<float, false><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, rf, h->c, zbeg,   \
+                                                             zstride);                                       \
+    }                                                                                                        \
+  } while (0)
+  if (h->p.model == LBM_MODEL_RM)
+    LBM_LAUNCH(k_collide_stream_raw);
+  else if (h->paper_rates)
+    LBM_LAUNCH(k_collide_stream_paper);
+  else
+    LBM_LAUNCH(k_collide_stream);
+#undef LBM_LAUNCH
   CU(cudaGetLastError());
   if (timed) {
     CU(cudaEventRecord(h->ev_t.back().second, s));
@@ -245,6 +262,19 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
     h->launches++;
     h->cs_launches++;
   }
+  return LBM_OK;
+}
+
+// FULL_FD density pass over planes zbeg + i*zstride of the local slab
+int launch_density(lbm_cuboid* h, const void* src, int zbeg, int nplanes, int zstride, cudaStream_t s) {
+  if (nplanes <= 0) return LBM_OK;
+  dim3 g = grid_for(h, nplanes);
+  if (h->p.precision == LBM_FP64)
+    lbm::k_density<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, h->d_rho, h->c, zbeg, zstride);
+  else
+    lbm::k_density<float><<<g, lbm::kBlock, 0, s>>>((const float*)src, h->d_rho, h->c, zbeg, zstride);
+  CU(cudaGetLastError());
+  if (!h->capturing) h->launches++;
   return LBM_OK;
 }
 
@@ -261,16 +291,21 @@ bool use_graphs(const lbm_cuboid* h) {
   return h->p.graphs == 2 || h->nxy * h->nzl < kGraphMaxNodes;
 }
 
+int step_once(lbm_cuboid* h);
+
 // capture kGraphSteps single-GPU steps starting from buffer `start`
 int capture_graph(lbm_cuboid* h, int start) {
   cudaGraph_t g = nullptr;
   CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   h->capturing = true;
-  int rc = LBM_OK, c = start;
+  int rc = LBM_OK;
+  const int cur0 = h->cur;
+  h->cur = start;
   for (int t = 0; t < kGraphSteps && rc == LBM_OK; ++t) {
-    rc = launch_cs(h, h->buf[c], h->buf[c ^ 1], 0, h->nzl, 1, h->stream);
-    c ^= 1;
+    rc = step_once(h);
+    h->cur ^= 1;  // kGraphSteps is even: ends on `start`
   }
+  h->cur = cur0;
   h->capturing = false;
   cudaError_t e = cudaStreamEndCapture(h->stream, &g);
   if (rc) {
@@ -337,6 +372,27 @@ int exchange(lbm_cuboid* h, int which) {
   return LBM_OK;
 }
 
+// FULL_FD: the density of the two boundary planes into the neighbours' ghost
+// planes (same peers and order as the population exchange), then the compute
+// stream waits for it.
+int exchange_rho(lbm_cuboid* h) {
+  if (!h->ghost) return LBM_OK;
+  CU(cudaEventRecord(h->ev_bnd, h->stream));
+  CU(cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
+  const HaloPlan hp = make_plan(&h->p);
+  const size_t n = size_t(h->nxy), nzl = size_t(h->nzl);
+  double* r = h->d_rho;
+  NC(ncclGroupStart());
+  if (hp.peer_up >= 0) NC(ncclSend(r + nzl * n, n, ncclDouble, hp.peer_up, h->comm, h->comm_stream));
+  if (hp.peer_down >= 0) NC(ncclRecv(r, n, ncclDouble, hp.peer_down, h->comm, h->comm_stream));
+  if (hp.peer_down >= 0) NC(ncclSend(r + n, n, ncclDouble, hp.peer_down, h->comm, h->comm_stream));
+  if (hp.peer_up >= 0) NC(ncclRecv(r + (nzl + 1) * n, n, ncclDouble, hp.peer_up, h->comm, h->comm_stream));
+  NC(ncclGroupEnd());
+  CU(cudaEventRecord(h->ev_rho, h->comm_stream));
+  CU(cudaStreamWaitEvent(h->stream, h->ev_rho, 0));
+  return LBM_OK;
+}
+
 int wait_halo(lbm_cuboid* h) {
   if (h->halo_pending) {
     CU(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
@@ -390,6 +446,29 @@ int run_macro(lbm_cuboid* h, double* rho, double* u, long long ustride, int zbeg
   CU(cudaGetLastError());
   h->launches++;
   return LBM_OK;
+}
+
+// Enqueue one time step from buf[cur] into buf[cur ^ 1] (does not flip cur).
+int step_once(lbm_cuboid* h) {
+  int rc;
+  void* src = h->buf[h->cur];
+  void* dst = h->buf[h->cur ^ 1];
+  if (!h->ghost) {
+    if (h->fd && (rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
+    return launch_cs(h, src, dst, 0, h->nzl, 1, h->stream);
+  }
+  if ((rc = wait_halo(h))) return rc;
+  if (h->fd) {
+    // same-time density of every local plane, then its boundary planes to the neighbours
+    if ((rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
+    if ((rc = exchange_rho(h))) return rc;
+  }
+  // both boundary planes first, in one launch (critical path of the exchange) ...
+  const int nb = (h->nzl > 1) ? 2 : 1;
+  if ((rc = launch_cs(h, src, dst, 0, nb, std::max(1, h->nzl - 1), h->stream))) return rc;
+  if ((rc = exchange(h, h->cur ^ 1))) return rc;
+  // ... then the interior, overlapping the NCCL transfer
+  return launch_cs(h, src, dst, 1, h->nzl - 2, 1, h->stream);
 }
 
 }  // namespace
@@ -459,6 +538,7 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->peer_up = hp.peer_up;
   h->peer_down = hp.peer_down;
   h->paper_rates = (p->omega_1 == 1.0 && p->omega_high == 1.0);
+  h->fd = (p->corrections == LBM_CORR_FULL_FD);
   fill_consts(h);
 
   auto bail = [&](int code) {
@@ -495,11 +575,17 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
       cudaMemsetAsync(h->d_dbg, 0, sizeof(unsigned int), h->stream) != cudaSuccess)
     return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
   h->c.dbg_flag = h->d_dbg;
+  if (h->fd) {
+    const size_t rb = size_t(h->nxy) * (h->nzl + 2) * sizeof(double);
+    if (cudaMalloc(&h->d_rho, rb) != cudaSuccess || cudaMemsetAsync(h->d_rho, 0, rb, h->stream) != cudaSuccess)
+      return bail(fail(LBM_ENOMEM, "cudaMalloc(%zu) for the density field failed", rb));
+  }
   if (h->ghost) {
     if (!p->nccl_uid) return bail(fail(LBM_EINVAL, "nccl_uid is required for the NCCL ghost exchange"));
     if (cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&h->ev_halo, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_rho, cudaEventDisableTiming) != cudaSuccess)
       return bail(fail(LBM_ECUDA, "stream/event creation failed"));
     ncclUniqueId id;
     std::memcpy(&id, p->nccl_uid, sizeof(id));
@@ -560,19 +646,7 @@ int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
     }
   }
   for (int64_t t = 0; t < nsteps; ++t) {
-    void* src = h->buf[h->cur];
-    void* dst = h->buf[h->cur ^ 1];
-    if (!h->ghost) {
-      if ((rc = launch_cs(h, src, dst, 0, h->nzl, 1, h->stream))) return rc;
-    } else {
-      if ((rc = wait_halo(h))) return rc;
-      // both boundary planes first, in one launch (critical path of the exchange) ...
-      const int nb = (h->nzl > 1) ? 2 : 1;
-      if ((rc = launch_cs(h, src, dst, 0, nb, std::max(1, h->nzl - 1), h->stream))) return rc;
-      if ((rc = exchange(h, h->cur ^ 1))) return rc;
-      // ... then the interior, overlapping the NCCL transfer
-      if ((rc = launch_cs(h, src, dst, 1, h->nzl - 2, 1, h->stream))) return rc;
-    }
+    if ((rc = step_once(h))) return rc;
     h->cur ^= 1;
     h->steps++;
   }
@@ -776,6 +850,8 @@ int lbm_cuboid_destroy(lbm_cuboid_t* h) {
   if (h->stage) cudaFree(h->stage);
   if (h->d_check) cudaFree(h->d_check);
   if (h->d_dbg) cudaFree(h->d_dbg);
+  if (h->d_rho) cudaFree(h->d_rho);
+  if (h->ev_rho) cudaEventDestroy(h->ev_rho);
   clear_timing(h);
   drop_graphs(h);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

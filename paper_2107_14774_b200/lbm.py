@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("LBM_CUBOID_LIB", os.path.join(_PKG, "liblbm_cuboid.so
 
 LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EUNSTABLE, LBM_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
 BC_PERIODIC, BC_BOUNCE_BACK, BC_MOVING_WALL, BC_FREE_SLIP = 0, 1, 2, 3
-CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF = 0, 1, 2
+CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF, CORR_FULL_FD = 0, 1, 2, 3
 FP64, FP32_STORAGE = 0, 1
 HALO_AUTO, HALO_NCCL = 0, 1
 MODEL_CM, MODEL_RM = 0, 1

@@ -341,3 +341,45 @@ def test_parity_time_periodic_force(P):
     ro, uo = o.macroscopic()
     rg, ug = g.get_macroscopic()
     assert np.abs(ro - rg).max() < 1e-12 and np.abs(uo - ug).max() < 1e-12
+
+
+# ------------------------------------------------- FULL_FD (density-gradient terms)
+@pytest.mark.parametrize("model", [0, 1])
+@pytest.mark.parametrize("name", ["tgv_full", "cavity100", "shear", "duct"])
+def test_parity_full_fd(P, name, model):
+    w = CASES[name].scaled(corrections=synth.CORR_FULL_FD, model=model)
+    o, g = _init_both(P, w, seed=53)
+    o.step(60)
+    g.step(60)
+    _cmp(o, g)
+
+
+def test_parity_full_fd_generic_rates_fp32(P):
+    w = synth.Workload("fd-generic", 15, 9, 8, r=0.75, s=1.3, nu=0.02, omega_xi=1.3, omega_1=1.2,
+                       omega_high=0.9, force=(1e-5, 0.0, -2e-5), corrections=synth.CORR_FULL_FD,
+                       init="random", seed=9)
+    o, g = _init_both(P, w, seed=9, noneq=1e-3)
+    o.step(40)
+    g.step(40)
+    _cmp(o, g)
+    w32 = w.scaled(precision=synth.PREC_FP32)
+    o, g = _init_both(P, w32, seed=9)
+    o.step(40)
+    g.step(40)
+    _cmp(o, g, prec=1)
+
+
+def test_full_fd_nccl_halo_and_graphs_bitwise(P):
+    """FULL_FD through the ghost-plane path (density planes exchanged by NCCL,
+    send to self) and through CUDA graphs equals the plain single-GPU launches."""
+    w = CASES["weak_tgv"].scaled(corrections=synth.CORR_FULL_FD)
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 57)
+    a = _gpu(P, w, graphs=1)
+    b = _gpu(P, w, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id())
+    c = _gpu(P, w, graphs=2)
+    for g in (a, b, c):
+        g.init_fields(rho, u)
+        g.step(70)
+    fa = a.get_populations()
+    assert np.array_equal(fa, b.get_populations())
+    assert np.array_equal(fa, c.get_populations())
