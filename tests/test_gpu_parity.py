@@ -383,3 +383,76 @@ def test_full_fd_nccl_halo_and_graphs_bitwise(P):
     fa = a.get_populations()
     assert np.array_equal(fa, b.get_populations())
     assert np.array_equal(fa, c.get_populations())
+
+
+def _patch_update(w, rho_g, u_g, x, y, z):
+    """Oracle value after ONE step of node (x, y, z) of the full grid: a 3x3x3
+    patch of the initial fields holding all the node's pull sources.  Along a
+    periodic axis the patch wraps around the node; along an axis where the node
+    touches a wall the patch starts at that wall and keeps its boundary type."""
+    import oracle as O
+
+    n = (w.nx, w.ny, w.nz)
+    pos = (x, y, z)
+    idx, centre, bc = [], [], list(w.bc)
+    for d in range(3):
+        lo_wall = w.bc[2 * d] != synth.BC_PERIODIC
+        if lo_wall and pos[d] == 0:
+            ids, c = [0, 1, 2], 0
+        elif lo_wall and pos[d] == n[d] - 1:
+            ids, c = [n[d] - 3, n[d] - 2, n[d] - 1], 2
+        else:
+            ids, c = [(pos[d] + k) % n[d] for k in (-1, 0, 1)], 1
+            bc[2 * d] = bc[2 * d + 1] = synth.BC_PERIODIC
+        idx.append(ids)
+        centre.append(c)
+    d = w.params()
+    d.update(nx=3, ny=3, nz=3, bc=tuple(bc))
+    o = O.Oracle(**d)
+    sel = np.ix_(idx[2], idx[1], idx[0])
+    o.init_fields(rho_g[sel], np.stack([u_g[k][sel] for k in range(3)]))
+    o.step(1)
+    return o.get_populations()[:, centre[2], centre[1], centre[0]]
+
+
+def test_full_size_config4_shear_layer_sampled(P):
+    """BASELINE config 4 at full size (512x256x512, r=0.5, s=1, free-slip y walls,
+    tanh profile + seeded noise): one step on the GPU, sampled nodes including
+    both free-slip walls against the oracle's patch update."""
+    w = synth.CONFIGS["shear"]
+    rho, u = synth.initial_fields(w)
+    g = _gpu(P, w)
+    g.init_fields(rho, u)
+    g.step(1)
+    rng = np.random.default_rng(2)
+    for z in (0, 300, 511):
+        fz = g.get_populations_planes(z, 1)[:, 0]
+        ys = np.concatenate([[0, 0, w.ny - 1, w.ny - 1, 1, w.ny - 2], rng.integers(0, w.ny, 4)])
+        xs = np.concatenate([[0, w.nx - 1, 0, w.nx - 1, 7, 9], rng.integers(0, w.nx, 4)])
+        for x, y in zip(xs, ys):
+            ref = _patch_update(w, rho, u, x, y, z)
+            assert np.abs(fz[:, y, x] - ref).max() <= TOL64
+    d = g.check()
+    assert d["bad_nodes"] == 0
+
+
+def test_full_size_config3_cavity_properties(P):
+    """BASELINE config 3 at full size (256x256x128, s = 2, Re = 1000): properties
+    that hold at any size -- total mass is conserved to round-off with all walls,
+    and the z-mirror symmetry of the lid-driven box is kept (u_z odd, u_x, u_y
+    even about the mid-plane) after 2000 steps."""
+    w = synth.CONFIGS["cavity1000"]
+    g = _gpu(P, w)
+    rho, u = synth.rest_fields(w.nx, w.ny, w.nz)
+    g.init_fields(rho, u)
+    m0 = g.check()["mass"]
+    g.step(2000)
+    d = g.check()
+    assert d["bad_nodes"] == 0 and abs(d["mass"] - m0) / m0 < 1e-11
+    assert 0.3 * w.wall_u < d["max_speed"] < 1.5 * w.wall_u
+    _, uu = g.get_macroscopic()
+    mir = uu[:, ::-1]
+    scale = w.wall_u
+    assert np.abs(uu[0] - mir[0]).max() < 1e-9 * scale
+    assert np.abs(uu[1] - mir[1]).max() < 1e-9 * scale
+    assert np.abs(uu[2] + mir[2]).max() < 1e-9 * scale
