@@ -41,7 +41,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
-    ap.add_argument("--workload", default="weak", choices=["weak", "shear", "cavity100", "cavity1000", "tgv"])
+    ap.add_argument("--workload", default="weak", choices=["weak", "strong", "shear", "cavity100", "cavity1000", "tgv"])
+    ap.add_argument("--streaming", choices=["ab", "aa"], default="ab",
+                    help="aa: one population buffer updated in place (single GPU)")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -220,6 +222,8 @@ def run_cuda(args):
     w = workload(args, world)
     z0, z1 = synth.slab_range(w.nz, rank, world)
     kw = w.params()
+    if args.streaming == "aa":
+        kw["streaming"] = P.STREAM_AA
     if world > 1:
         lat = P.distributed_lattice(device=local, **kw)
     elif args.halo == "nccl":
@@ -329,6 +333,8 @@ def run_cuda(args):
     traffic = ncu_traffic(w.name, prec)
     kname = ("k_collide_stream_raw" if w.model == synth.MODEL_RM else
              "k_collide_stream_paper" if lat.info()["paper_rate_kernel"] else "k_collide_stream")
+    if args.streaming == "aa":
+        kname = "k_aa (odd/even)"
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "peak_source": peak_src,
             "kernel": f"{kname}<{'double' if prec == 'fp64' else 'float'}>",
@@ -349,9 +355,10 @@ def run_cuda(args):
             "config": {"workload": w.name, "grid_global": [w.nx, w.ny, w.nz], "nodes_global": w.nodes,
                        "r": w.r, "s": w.s, "nu": w.nu, "corrections": args.corrections.upper(),
                        "model": "3DCCM" if w.model == 0 else "3DCRM", "storage": prec,
-                       "l2": "working set per step (58 GB/GPU fp64) >> 126 MB L2; no flush needed",
+                       "l2": "working set per step >> 126 MB L2; no flush needed",
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
-                       "halo": "nccl ghost planes" if lat.info()["nccl_halo"] else "in-kernel wrap"},
+                       "halo": "nccl ghost planes" if lat.info()["nccl_halo"] else "in-kernel wrap",
+                       "streaming": "AA in place (1 buffer)" if args.streaming == "aa" else "AB (2 buffers)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "bad_nodes": bad}
     print(json.dumps(line), flush=True)

@@ -47,7 +47,7 @@ typedef enum {
   LBM_ECUDA = -3,     /* CUDA runtime error (message has the CUDA string) */
   LBM_ENCCL = -4,     /* NCCL error */
   LBM_EUNSTABLE = -5, /* NaN, rho <= 0 or |u| > 1 seen by lbm_cuboid_check() */
-  LBM_ENOTSUP = -6    /* built without the requested feature (e.g. NCCL) */
+  LBM_ENOTSUP = -6    /* unsupported parameter combination (e.g. AA streaming on several GPUs) */
 } lbm_status;
 
 /* Face boundary types.  Faces are ordered -x, +x, -y, +y, -z, +z.  Opposite
@@ -80,6 +80,15 @@ typedef enum {
   LBM_MODEL_RM = 1  /* 3DCRM-LBM: raw moments, same corrections (P:L642-648, L744(ii), L1011) */
 } lbm_model;
 
+/* Population storage / streaming pattern. */
+typedef enum {
+  LBM_STREAM_AB = 0, /* two buffers: pull from one, store into the other (default) */
+  LBM_STREAM_AA = 1  /* one buffer updated in place, alternating an "odd" step (pull from reversed
+                        slots, collide, push) and an "even" step (collide in place, store reversed):
+                        half the memory, same 2*27*sizeof(real) bytes per node update; single GPU,
+                        not with LBM_CORR_FULL_FD */
+} lbm_streaming;
+
 typedef enum {
   LBM_HALO_AUTO = 0, /* 1 GPU + periodic z: wrap inside the kernel; else NCCL ghost planes */
   LBM_HALO_NCCL = 1  /* always exchange ghost planes with NCCL (also world == 1: send to self) */
@@ -106,6 +115,7 @@ typedef struct {
                                   the slab has < 4M nodes and no ghost exchange), 1 never, 2 always
                                   (when no ghost exchange) */
   int32_t model;               /* lbm_model */
+  int32_t streaming;           /* lbm_streaming; with LBM_STREAM_AA only buf_a is used */
   const void *nccl_uid;        /* 128-byte ncclUniqueId from lbm_cuboid_nccl_unique_id() on rank 0,
                                   broadcast by the caller; required iff NCCL ghost exchange is used */
   void *stream;                /* cudaStream_t for all compute work; NULL -> library-owned stream */

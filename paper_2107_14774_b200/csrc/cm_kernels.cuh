@@ -276,9 +276,10 @@ __device__ __forceinline__ void collide_generic(const Consts& c, double (&f)[27]
 // -------------------------------------------------------------- streaming
 // Gather the 27 incoming populations of node (x, y, z) (pull form).
 // Fast path: no wall face adjacent -> periodic/ghost addressing only.
-template <typename T>
-__device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& c, int x, int y, int z,
-                                       double (&f)[27]) {
+// REV (AA odd steps): the source buffer holds f~_s(z) at slot 26 - s of node z.
+template <typename T, bool REV = false>
+__device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int y, int z, double (&f)[27]) {
+  auto slot = [](int s) { return REV ? 26 - s : s; };
   const int nx = c.nx;
   const int xm = (x == 0) ? nx - 1 : x - 1;        // source of e_x = +1
   const int xp = (x == nx - 1) ? 0 : x + 1;        // source of e_x = -1
@@ -309,7 +310,7 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
           const int q = LBM_Q(i, j, k);
-          f[q] = ldg(LBM_CHECK_LD(src, pz[k] + q * c.nxy + sy[j] + sx[i], c));
+          f[q] = ldg(LBM_CHECK_LD(src, pz[k] + slot(q) * c.nxy + sy[j] + sx[i], c));
         }
     return;
   }
@@ -341,7 +342,7 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
                             (kz == FK_BOUNCE || kz == FK_MOVING);
         if (noslip) {
           // halfway bounce-back from the own node's opposite direction
-          double v = ldg(LBM_CHECK_LD(src, p0 + LBM_Q(2 - i, 2 - j, 2 - k) * c.nxy + own, c));
+          double v = ldg(LBM_CHECK_LD(src, p0 + slot(LBM_Q(2 - i, 2 - j, 2 - k)) * c.nxy + own, c));
           if (ky == FK_MOVING)  // Eq. 69: + rho_f U e_x cs2/(2 r^2) phi_z(e_z)
             v = fma(rho_f * c.lid_u * (double)ex, c.lid_c[k], v);
           f[q] = v;
@@ -353,7 +354,7 @@ __device__ __forceinline__ void gather(const T* __restrict__ src, const Consts& 
           const int xs = mx ? x : sx[i];
           const int ys = my ? y * nx : sy[j];
           const T* zs = mz ? p0 : pz[k];
-          f[q] = ldg(LBM_CHECK_LD(src, zs + LBM_Q(qi, qj, qk) * c.nxy + ys + xs, c));
+          f[q] = ldg(LBM_CHECK_LD(src, zs + slot(LBM_Q(qi, qj, qk)) * c.nxy + ys + xs, c));
         }
       }
 }
@@ -414,29 +415,117 @@ __global__ void __launch_bounds__(kBlock) k_density(const T* __restrict__ src, d
   rho_out[(long long)(z + 1) * c.nxy + idx] = r0;
 }
 
-// --------------------------------------------------------- the fused kernel
-// One thread per node of planes zbeg + i*zstride, i < gridDim.y, of the local slab.
+// --------------------------------------------------------- store policies
+// Where the post-collision populations f~_q(x) go:
+//   StoreOwn  (two-buffer "AB" pull scheme): own node, slot q of the other buffer;
+//   StoreRev  (AA even step): own node, slot 26 - q of the same buffer;
+//   StorePush (AA odd step): the slot whose next pull reads it (push with the
+//             wall rules; the exact inverse of gather()).
+template <typename T>
+struct StoreOwn {
+  T* base;
+  T* out;
+  int nxy;
+  const Consts* c;
+  __device__ __forceinline__ void begin(double) {}
+  __device__ __forceinline__ void operator()(int q, double v) const {
+    stcs<T>(LBM_CHECK_ST(base, out + q * nxy, *c), v);
+  }
+};
+
+template <typename T>
+struct StoreRev {
+  T* base;
+  T* out;
+  int nxy;
+  const Consts* c;
+  __device__ __forceinline__ void begin(double) {}
+  __device__ __forceinline__ void operator()(int q, double v) const {
+    stcs<T>(LBM_CHECK_ST(base, out + (26 - q) * nxy, *c), v);
+  }
+};
+
+// Push: f~_q(x) goes to the population the next pull at x + e_q takes it from.
+// Normal link: node x + e_q (periodic wrap), slot q.  A crossed no-slip face:
+// own node, slot 26 - q, plus the Eq. 69 term if the face is the moving lid
+// (rho_f = rho of the node = sum f~, reading R4).  A crossed free-slip face:
+// node x + e'_q (crossed axes zeroed), slot q* (crossed axes mirrored).
+template <typename T>
+struct StorePush {
+  T* base;
+  const Consts* c;
+  int x, y, own;
+  int dx[3], dy[3];   // destination x, y*nx for displacement e + 1
+  T* pz[3];           // destination plane for e_z + 1
+  int cx[3], cy[3], cz[3];  // kind of the face crossed by displacement e + 1 (0: none)
+  bool wall;
+  double rho_f;
+  __device__ __forceinline__ StorePush(T* buf, const Consts& cc, int x_, int y_, int z) : base(buf), c(&cc), x(x_), y(y_) {
+    const int nx = cc.nx;
+    own = y * nx + x;
+    dx[0] = (x == 0) ? nx - 1 : x - 1;
+    dx[1] = x;
+    dx[2] = (x == nx - 1) ? 0 : x + 1;
+    dy[0] = ((y == 0) ? cc.ny - 1 : y - 1) * nx;
+    dy[1] = y * nx;
+    dy[2] = ((y == cc.ny - 1) ? 0 : y + 1) * nx;
+    const int zm = (z == 0) ? cc.nzl - 1 : z - 1, zp = (z == cc.nzl - 1) ? 0 : z + 1;
+    pz[0] = buf + (long long)(zm + 1) * cc.plane;
+    pz[1] = buf + (long long)(z + 1) * cc.plane;
+    pz[2] = buf + (long long)(zp + 1) * cc.plane;
+    auto kind = [](int fk) { return (fk >= FK_BOUNCE && fk <= FK_SLIP) ? fk : 0; };
+    cx[0] = (x == 0) ? kind(cc.face[0]) : 0;
+    cx[1] = 0;
+    cx[2] = (x == nx - 1) ? kind(cc.face[1]) : 0;
+    cy[0] = (y == 0) ? kind(cc.face[2]) : 0;
+    cy[1] = 0;
+    cy[2] = (y == cc.ny - 1) ? kind(cc.face[3]) : 0;
+    cz[0] = (z == 0) ? kind(cc.face[4]) : 0;
+    cz[1] = 0;
+    cz[2] = (z == cc.nzl - 1) ? kind(cc.face[5]) : 0;
+    wall = cx[0] | cx[2] | cy[0] | cy[2] | cz[0] | cz[2];
+    rho_f = 0.0;
+  }
+  __device__ __forceinline__ void begin(double rho) { rho_f = rho; }
+  __device__ __forceinline__ void operator()(int q, double v) const {
+    const int i = q % 3, j = (q / 3) % 3, k = q / 9;
+    const int nxy = c->nxy;
+    if (!wall) {
+      stcs<T>(LBM_CHECK_ST(base, pz[k] + q * nxy + dy[j] + dx[i], *c), v);
+      return;
+    }
+    const int kx = cx[i], ky = cy[j], kz = cz[k];
+    const bool noslip = (kx == FK_BOUNCE || kx == FK_MOVING) || (ky == FK_BOUNCE || ky == FK_MOVING) ||
+                        (kz == FK_BOUNCE || kz == FK_MOVING);
+    if (noslip) {
+      double w = v;
+      if (ky == FK_MOVING)  // arrives as direction 26 - q: + rho_f U e_x(26-q) lid_c[e_z(26-q)]
+        w = fma(rho_f * c->lid_u * (double)(1 - i), c->lid_c[2 - k], w);
+      stcs<T>(LBM_CHECK_ST(base, pz[1] + (26 - q) * nxy + own, *c), w);
+    } else {
+      const bool mx = (kx == FK_SLIP), my = (ky == FK_SLIP), mz = (kz == FK_SLIP);
+      const int qi = mx ? 2 - i : i, qj = my ? 2 - j : j, qk = mz ? 2 - k : k;
+      const int xs = mx ? x : dx[i];
+      const int ys = my ? y * c->nx : dy[j];
+      T* zs = mz ? pz[1] : pz[k];
+      stcs<T>(LBM_CHECK_ST(base, zs + LBM_Q(qi, qj, qk) * nxy + ys + xs, *c), v);
+    }
+  }
+};
+
+// ------------------------------------------------------------ collision cores
+// Each core takes the 27 pre-collision populations f (internal order) of one
+// node and hands the 27 post-collision populations to the store policy.
 #if LBM_MINB > 0
 #define LBM_CS_BOUNDS __launch_bounds__(kBlock, LBM_MINB)
 #else
 #define LBM_CS_BOUNDS __launch_bounds__(kBlock)
 #endif
-template <typename T, bool FD>
-__global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __restrict__ dst,
-                                               const double* __restrict__ rf, const __grid_constant__ Consts c,
-                                               int zbeg, int zstride) {
-  const int idx = blockIdx.x * kBlock + threadIdx.x;
-  if (idx >= c.nxy) return;
-  const int y = idx / c.nx;
-  const int x = idx - y * c.nx;
-  const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
 
-  double f[27];
-  // FULL_FD: gradient first, so its L2-resident loads overlap the population loads
-  double gxr = 0.0, gyr = 0.0, gzr = 0.0;
-  if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
-  gather<T>(src, c, x, y, z, f);
-
+// Generic rates (any omega_1, omega_high): all 27 central moments.
+template <bool FD, class St>
+__device__ __forceinline__ void core_generic(const Consts& c, double (&f)[27], double gxr, double gyr, double gzr,
+                                             St& st) {
   // m = P f (App A), per axis
   raw_pass<0>(f);
   raw_pass<1>(f);
@@ -458,10 +547,9 @@ __global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __r
   inverse_pass<2>(f, uz, c.h1z, c.h2z);
   inverse_pass<1>(f, uy, c.h1y, c.h2y);
   inverse_pass<0>(f, ux, 0.5, 0.5);
-
-  T* out = dst + (long long)(z + 1) * c.plane + idx;
+  st.begin(rho);
 #pragma unroll
-  for (int q = 0; q < 27; ++q) stcs<T>(LBM_CHECK_ST(dst, out + q * c.nxy, c), f[q]);
+  for (int q = 0; q < 27; ++q) st(q, f[q]);
 }
 
 // ------------------------------------- paper-rate kernel (omega_1 = omega_high = 1)
@@ -490,22 +578,9 @@ __device__ __forceinline__ void inv1d(double k0, double k1, double k2, double u,
   fp = t2 + t1;
 }
 
-template <typename T, bool FD>
-__global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, T* __restrict__ dst,
-                                                     const double* __restrict__ rf, const __grid_constant__ Consts c,
-                                                     int zbeg, int zstride) {
-  const int idx = blockIdx.x * kBlock + threadIdx.x;
-  if (idx >= c.nxy) return;
-  const int y = idx / c.nx;
-  const int x = idx - y * c.nx;
-  const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
-
-  double f[27];
-  // FULL_FD: gradient first, so its L2-resident loads overlap the population loads
-  double gxr = 0.0, gyr = 0.0, gzr = 0.0;
-  if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
-  gather<T>(src, c, x, y, z, f);
-
+template <bool FD, class St>
+__device__ __forceinline__ void core_paper(const Consts& c, double (&f)[27], double gxr, double gyr, double gzr,
+                                           St& st) {
   // raw moments up to second order, cubic units (App A restricted to m+n+p <= 2).
   // x-pass on all nine (y,z) rows: slots (0,j,k), (1,j,k), (2,j,k) <- m0, m1, m2 along x
   raw_pass<0>(f);
@@ -571,7 +646,7 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, 
   inv1d<false, true>(K020, 0.0, c4r, uz, c.h1z, c.h2z, G02[0], G02[1], G02[2]);
   inv1d<false, true>(c4r, 0.0, c6r, uz, c.h1z, c.h2z, G22[0], G22[1], G22[2]);
 
-  T* out = dst + (long long)(z + 1) * c.plane + idx;
+  st.begin(rho);
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     // y: (x-order 0): (G00, G01, G02); (x-order 1): (G10, G11, 0); (x-order 2): (G20, 0, G22)
@@ -583,9 +658,9 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, 
     for (int j = 0; j < 3; ++j) {
       double fm, f0, fp;
       inv1d<true, true>(H0[j], H1[j], H2[j], ux, 0.5, 0.5, fm, f0, fp);
-      stcs<T>(LBM_CHECK_ST(dst, out + LBM_Q(0, j, k) * c.nxy, c), fm);
-      stcs<T>(LBM_CHECK_ST(dst, out + LBM_Q(1, j, k) * c.nxy, c), f0);
-      stcs<T>(LBM_CHECK_ST(dst, out + LBM_Q(2, j, k) * c.nxy, c), fp);
+      st(LBM_Q(0, j, k), fm);
+      st(LBM_Q(1, j, k), f0);
+      st(LBM_Q(2, j, k), fp);
     }
   }
 }
@@ -706,20 +781,9 @@ __device__ __forceinline__ void collide_raw(const Consts& c, double (&f)[27], do
 #undef M
 }
 
-template <typename T, bool FD>
-__global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T* __restrict__ dst,
-                                                   const double* __restrict__ rf, const __grid_constant__ Consts c,
-                                                   int zbeg, int zstride) {
-  const int idx = blockIdx.x * kBlock + threadIdx.x;
-  if (idx >= c.nxy) return;
-  const int y = idx / c.nx;
-  const int x = idx - y * c.nx;
-  const int z = zbeg + blockIdx.y * zstride;
-  double f[27];
-  // FULL_FD: gradient first, so its L2-resident loads overlap the population loads
-  double gxr = 0.0, gyr = 0.0, gzr = 0.0;
-  if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
-  gather<T>(src, c, x, y, z, f);
+template <bool FD, class St>
+__device__ __forceinline__ void core_raw(const Consts& c, double (&f)[27], double gxr, double gyr, double gzr,
+                                         St& st) {
   raw_pass<0>(f);
   raw_pass<1>(f);
   raw_pass<2>(f);
@@ -734,9 +798,137 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T*
   unscale_inverse_pass<2>(f, c.h1z, c.h2z);
   unscale_inverse_pass<1>(f, c.h1y, c.h2y);
   unscale_inverse_pass<0>(f, 0.5, 0.5);
-  T* out = dst + (long long)(z + 1) * c.plane + idx;
+  st.begin(rho);
 #pragma unroll
-  for (int q = 0; q < 27; ++q) stcs<T>(LBM_CHECK_ST(dst, out + q * c.nxy, c), f[q]);
+  for (int q = 0; q < 27; ++q) st(q, f[q]);
+}
+
+enum CoreKind : int { CORE_GENERIC = 0, CORE_PAPER = 1, CORE_RAW = 2 };
+
+template <int KIND, bool FD, class St>
+__device__ __forceinline__ void run_core(const Consts& c, double (&f)[27], double gxr, double gyr, double gzr,
+                                         St& st) {
+  if (KIND == CORE_PAPER)
+    core_paper<FD>(c, f, gxr, gyr, gzr, st);
+  else if (KIND == CORE_RAW)
+    core_raw<FD>(c, f, gxr, gyr, gzr, st);
+  else
+    core_generic<FD>(c, f, gxr, gyr, gzr, st);
+}
+
+// ------------------------------------------------ the fused kernels (two buffers)
+// One thread per node of planes zbeg + i*zstride, i < gridDim.y, of the local
+// slab: pull (gather) from src, collide, store at the own node of dst.
+template <typename T, int KIND, bool FD>
+__device__ __forceinline__ void collide_stream_ab(const T* __restrict__ src, T* __restrict__ dst,
+                                                  const double* __restrict__ rf, const Consts& c, int zbeg,
+                                                  int zstride) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int y = idx / c.nx;
+  const int x = idx - y * c.nx;
+  const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
+  double f[27];
+  // FULL_FD: gradient first, so its L2-resident loads overlap the population loads
+  double gxr = 0.0, gyr = 0.0, gzr = 0.0;
+  if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
+  gather<T>(src, c, x, y, z, f);
+  StoreOwn<T> st{dst, dst + (long long)(z + 1) * c.plane + idx, c.nxy, &c};
+  run_core<KIND, FD>(c, f, gxr, gyr, gzr, st);
+}
+
+template <typename T, bool FD>
+__global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __restrict__ dst,
+                                               const double* __restrict__ rf, const __grid_constant__ Consts c,
+                                               int zbeg, int zstride) {
+  collide_stream_ab<T, CORE_GENERIC, FD>(src, dst, rf, c, zbeg, zstride);
+}
+
+template <typename T, bool FD>
+__global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, T* __restrict__ dst,
+                                                     const double* __restrict__ rf, const __grid_constant__ Consts c,
+                                                     int zbeg, int zstride) {
+  collide_stream_ab<T, CORE_PAPER, FD>(src, dst, rf, c, zbeg, zstride);
+}
+
+template <typename T, bool FD>
+__global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T* __restrict__ dst,
+                                                   const double* __restrict__ rf, const __grid_constant__ Consts c,
+                                                   int zbeg, int zstride) {
+  collide_stream_ab<T, CORE_RAW, FD>(src, dst, rf, c, zbeg, zstride);
+}
+
+// ------------------------------------------------ AA in-place streaming (one buffer)
+// Layout R: slot 26 - q of node x holds f~_q(x) (post-collision, canonical);
+// layout N: slot q of node x holds f_q(x) (pre-collision, already streamed).
+//   odd step  (R -> N): gather through the wall rules from layout R (REV slots),
+//                       collide, push through the wall rules into layout N;
+//   even step (N -> R): load the own slots, collide, store reversed.
+// Each memory location is read and written only by the thread of one node, which
+// reads all its 27 values before writing any (the pull map is a bijection), so
+// the update is race-free in place.  Single-GPU only (no ghost planes).
+template <typename T, int KIND, bool ODD>
+__global__ void LBM_CS_BOUNDS k_aa(T* buf, const __grid_constant__ Consts c, int zbeg, int zstride) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int y = idx / c.nx;
+  const int x = idx - y * c.nx;
+  const int z = zbeg + blockIdx.y * zstride;
+  double f[27];
+  if (ODD) {
+    gather<T, true>(buf, c, x, y, z, f);
+    StorePush<T> st(buf, c, x, y, z);
+    run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, st);
+  } else {
+    T* p = buf + (long long)(z + 1) * c.plane + idx;
+#pragma unroll
+    for (int q = 0; q < 27; ++q) f[q] = ldg(LBM_CHECK_LD(buf, p + q * c.nxy, c));
+    StoreRev<T> st{buf, p, c.nxy, &c};
+    run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, st);
+  }
+}
+
+// Canonical post-collision populations f~_q(x) of node x from an AA buffer:
+// phase R: slot 26 - q; phase N: the slot the push wrote (minus the Eq. 69 term
+// on lid links; the nine lid terms sum to zero, so rho_f = sum of the values).
+template <typename T>
+__device__ __forceinline__ void aa_canonical(const T* buf, const Consts& c, int x, int y, int z, int phase,
+                                             double (&f)[27]) {
+  if (phase == 1) {
+    const T* p = buf + (long long)(z + 1) * c.plane + y * c.nx + x;
+#pragma unroll
+    for (int q = 0; q < 27; ++q) f[q] = ldg(p + (26 - q) * c.nxy);
+    return;
+  }
+  StorePush<T> d(const_cast<T*>(buf), c, x, y, z);
+  double rho_f = 0.0;
+  bool lid[27];
+#pragma unroll
+  for (int q = 0; q < 27; ++q) {
+    const int i = q % 3, j = (q / 3) % 3, k = q / 9;
+    const T* a;
+    lid[q] = false;
+    if (!d.wall) {
+      a = d.pz[k] + q * c.nxy + d.dy[j] + d.dx[i];
+    } else {
+      const int kx = d.cx[i], ky = d.cy[j], kz = d.cz[k];
+      const bool noslip = (kx == FK_BOUNCE || kx == FK_MOVING) || (ky == FK_BOUNCE || ky == FK_MOVING) ||
+                          (kz == FK_BOUNCE || kz == FK_MOVING);
+      if (noslip) {
+        a = d.pz[1] + (26 - q) * c.nxy + d.own;
+        lid[q] = (ky == FK_MOVING);
+      } else {
+        const bool mx = (kx == FK_SLIP), my = (ky == FK_SLIP), mz = (kz == FK_SLIP);
+        const int qi = mx ? 2 - i : i, qj = my ? 2 - j : j, qk = mz ? 2 - k : k;
+        a = (mz ? d.pz[1] : d.pz[k]) + LBM_Q(qi, qj, qk) * c.nxy + (my ? y * c.nx : d.dy[j]) + (mx ? x : d.dx[i]);
+      }
+    }
+    f[q] = ldg(a);
+    rho_f += f[q];
+  }
+#pragma unroll
+  for (int q = 0; q < 27; ++q)
+    if (lid[q]) f[q] -= rho_f * c.lid_u * (double)(1 - q % 3) * c.lid_c[2 - q / 9];
 }
 
 // -------------------------------------------------------------- init kernel
@@ -755,7 +947,7 @@ __device__ __forceinline__ void axis_phi(double u, double c, double cs2, double 
 template <typename T>
 __global__ void __launch_bounds__(kBlock) k_init(const double* __restrict__ rho_in, const double* __restrict__ u_in,
                                                  long long ustride, T* __restrict__ dst,
-                                                 const __grid_constant__ Consts c, int zbeg) {
+                                                 const __grid_constant__ Consts c, int zbeg, int rev) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
   const long long n = (long long)blockIdx.y * c.nxy + idx;
@@ -773,18 +965,36 @@ __global__ void __launch_bounds__(kBlock) k_init(const double* __restrict__ rho_
 #pragma unroll
     for (int j = 0; j < 3; ++j)
 #pragma unroll
-      for (int i = 0; i < 3; ++i) stcs<T>(out + LBM_Q(i, j, k) * c.nxy, rho * px[i] * py[j] * pz[k]);
+      for (int i = 0; i < 3; ++i) {
+        const int q = LBM_Q(i, j, k);
+        stcs<T>(out + (rev ? 26 - q : q) * c.nxy, rho * px[i] * py[j] * pz[k]);
+      }
 }
 
 // -------------------------------------------------------- macroscopic kernel
 // rho = sum f~, u = (sum f~ e - F/2)/rho of the stored post-collision state.
+// aa: 0 two-buffer layout, 1 AA phase R, 2 AA phase N (see aa_canonical)
+template <typename T>
+__device__ __forceinline__ void load_canonical(const T* src, const Consts& c, int idx, int z, int aa,
+                                               double (&f)[27]) {
+  if (aa == 0) {
+    const T* p = src + (long long)(z + 1) * c.plane + idx;
+#pragma unroll
+    for (int q = 0; q < 27; ++q) f[q] = ldg(p + q * c.nxy);
+  } else {
+    const int y = idx / c.nx;
+    aa_canonical<T>(src, c, idx - y * c.nx, y, z, aa == 1 ? 1 : 2, f);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(kBlock) k_macro(const T* __restrict__ src, double* __restrict__ rho_out,
                                                   double* __restrict__ u_out, long long ustride,
-                                                  const __grid_constant__ Consts c, int zbeg) {
+                                                  const __grid_constant__ Consts c, int zbeg, int aa) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
-  const T* p = src + (long long)(zbeg + blockIdx.y + 1) * c.plane + idx;
+  double f[27];
+  load_canonical<T>(src, c, idx, zbeg + blockIdx.y, aa, f);
   double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
@@ -792,7 +1002,7 @@ __global__ void __launch_bounds__(kBlock) k_macro(const T* __restrict__ src, dou
     for (int j = 0; j < 3; ++j)
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        const double v = ldg(p + LBM_Q(i, j, k) * c.nxy);
+        const double v = f[LBM_Q(i, j, k)];
         rho += v;
         jx += (double)(i - 1) * v;
         jy += (double)(j - 1) * v;
@@ -815,23 +1025,26 @@ __constant__ int8_t kPaperToInternal[27] = {
 
 template <typename T>
 __global__ void __launch_bounds__(kBlock) k_pack(const T* __restrict__ src, double* __restrict__ stage, int nplanes,
-                                                 const __grid_constant__ Consts c, int zbeg) {
+                                                 const __grid_constant__ Consts c, int zbeg, int aa) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
   const int zz = blockIdx.y;
-  const T* p = src + (long long)(zbeg + zz + 1) * c.plane + idx;
-  for (int a = 0; a < 27; ++a)
-    stage[((long long)a * nplanes + zz) * c.nxy + idx] = ldg(p + kPaperToInternal[a] * c.nxy);
+  double f[27];
+  load_canonical<T>(src, c, idx, zbeg + zz, aa, f);
+  for (int a = 0; a < 27; ++a) stage[((long long)a * nplanes + zz) * c.nxy + idx] = f[kPaperToInternal[a]];
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kBlock) k_unpack(const double* __restrict__ stage, T* __restrict__ dst, int nplanes,
-                                                   const __grid_constant__ Consts c, int zbeg) {
+                                                   const __grid_constant__ Consts c, int zbeg, int rev) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
   const int zz = blockIdx.y;
   T* p = dst + (long long)(zbeg + zz + 1) * c.plane + idx;
-  for (int a = 0; a < 27; ++a) p[kPaperToInternal[a] * c.nxy] = (T)stage[((long long)a * nplanes + zz) * c.nxy + idx];
+  for (int a = 0; a < 27; ++a) {
+    const int q = kPaperToInternal[a];
+    p[(rev ? 26 - q : q) * c.nxy] = (T)stage[((long long)a * nplanes + zz) * c.nxy + idx];
+  }
 }
 
 // -------------------------------------------------------------- check kernel
@@ -850,15 +1063,17 @@ __device__ __forceinline__ double warp_max(double v) {
 
 template <typename T>
 __global__ void __launch_bounds__(kBlock) k_check(const T* __restrict__ src, double* __restrict__ out,
-                                                  const __grid_constant__ Consts c) {
+                                                  const __grid_constant__ Consts c, int aa) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   const int z = blockIdx.y;
   double v[7] = {0, 0, 0, 0, 0, 0, 0};
   if (idx < c.nxy) {
-    const T* p = src + (long long)(z + 1) * c.plane + idx;
+    double fq[27];
+    load_canonical<T>(src, c, idx, z, aa, fq);
     double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
+#pragma unroll
     for (int q = 0; q < 27; ++q) {
-      const double fv = ldg(p + q * c.nxy);
+      const double fv = fq[q];
       const int i = q % 3, j = (q / 3) % 3, k = q / 9;
       rho += fv;
       jx += (i - 1) * fv;

@@ -76,6 +76,7 @@ struct lbm_cuboid {
   bool ghost = false;  // ghost-plane (NCCL) mode
   bool paper_rates = false;  // omega_1 = omega_high = 1 -> k_collide_stream_paper
   bool fd = false;           // FULL_FD: density pass + isotropic gradient
+  bool aa = false;           // AA in-place streaming: one buffer; cur = 0 layout R, cur = 1 layout N
   double* d_rho = nullptr;   // FULL_FD density field, population-buffer plane structure (ghost planes)
   cudaEvent_t ev_rho = nullptr;
   ncclComm_t comm = nullptr;
@@ -129,6 +130,13 @@ int validate(const lbm_cuboid_params* p) {
   if (p->halo < 0 || p->halo > 1) return fail(LBM_EINVAL, "halo must be an lbm_halo");
   if (p->graphs < 0 || p->graphs > 2) return fail(LBM_EINVAL, "graphs must be 0, 1 or 2");
   if (p->model < 0 || p->model > 1) return fail(LBM_EINVAL, "model must be an lbm_model");
+  if (p->streaming < 0 || p->streaming > 1) return fail(LBM_EINVAL, "streaming must be an lbm_streaming");
+  if (p->streaming == LBM_STREAM_AA) {
+    if (p->world > 1 || p->halo == LBM_HALO_NCCL)
+      return fail(LBM_ENOTSUP, "AA in-place streaming is single-GPU only (no ghost-plane exchange)");
+    if (p->corrections == LBM_CORR_FULL_FD)
+      return fail(LBM_ENOTSUP, "AA in-place streaming does not support FULL_FD");
+  }
   for (int d = 0; d < 3; ++d)
     if (!std::isfinite(p->force[d])) return fail(LBM_EINVAL, "force must be finite");
   if (!std::isfinite(p->wall_u)) return fail(LBM_EINVAL, "wall_u must be finite");
@@ -264,6 +272,52 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
   }
   return LBM_OK;
 }
+
+// AA in-place step over the whole slab: odd kernel from layout R (cur == 0),
+// even kernel from layout N (cur == 1)
+int launch_aa(lbm_cuboid* h, cudaStream_t s) {
+  dim3 g = grid_for(h, h->nzl);
+  const bool fp64 = (h->p.precision == LBM_FP64), odd = (h->cur == 0);
+  const int kind = (h->p.model == LBM_MODEL_RM) ? lbm::CORE_RAW : (h->paper_rates ? lbm::CORE_PAPER : lbm::CORE_GENERIC);
+  const bool timed = h->timing && h->ev_t.size() < kMaxTimedLaunches;
+  if (timed) {
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    h->ev_t.push_back({a, b});
+    CU(cudaEventRecord(a, s));
+  }
+#define LBM_AA(T, K)                                                                                   \
+  do {                                                                                                 \
+    if (odd)                                                                                           \
+      lbm::k_aa<T, K, true><<<g, lbm::kBlock, 0, s>>>((T*)h->buf[0], h->c, 0, 1);                    \
+    else                                                                                               \
+      lbm::k_aa<T, K, false><<<g, lbm::kBlock, 0, s>>>((T*)h->buf[0], h->c, 0, 1);                   \
+  } while (0)
+  if (fp64) {
+    if (kind == lbm::CORE_PAPER) LBM_AA(double, lbm::CORE_PAPER);
+    else if (kind == lbm::CORE_RAW) LBM_AA(double, lbm::CORE_RAW);
+    else LBM_AA(double, lbm::CORE_GENERIC);
+  } else {
+    if (kind == lbm::CORE_PAPER) LBM_AA(float, lbm::CORE_PAPER);
+    else if (kind == lbm::CORE_RAW) LBM_AA(float, lbm::CORE_RAW);
+    else LBM_AA(float, lbm::CORE_GENERIC);
+  }
+#undef LBM_AA
+  CU(cudaGetLastError());
+  if (timed) {
+    CU(cudaEventRecord(h->ev_t.back().second, s));
+    h->ev_t_nodes.push_back(int64_t(h->nzl) * h->nxy);
+  }
+  if (!h->capturing) {
+    h->launches++;
+    h->cs_launches++;
+  }
+  return LBM_OK;
+}
+
+// layout selector of the diagnostic kernels: 0 two-buffer, 1 AA layout R, 2 AA layout N
+int aa_mode(const lbm_cuboid* h) { return h->aa ? (h->cur == 0 ? 1 : 2) : 0; }
 
 // FULL_FD density pass over planes zbeg + i*zstride of the local slab
 int launch_density(lbm_cuboid* h, const void* src, int zbeg, int nplanes, int zstride, cudaStream_t s) {
@@ -425,7 +479,8 @@ int chunk_planes(const lbm_cuboid* h, int per_node) {
 
 template <typename T>
 int init_kernel(lbm_cuboid* h, const double* rho, const double* u, long long ustride, int zbeg, int n) {
-  lbm::k_init<T><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>(rho, u, ustride, (T*)h->buf[h->cur], h->c, zbeg);
+  lbm::k_init<T><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>(rho, u, ustride, (T*)h->buf[h->cur], h->c, zbeg,
+                                                                 h->aa ? 1 : 0);
   CU(cudaGetLastError());
   h->launches++;
   return LBM_OK;
@@ -439,10 +494,10 @@ int run_init(lbm_cuboid* h, const double* rho, const double* u, long long ustrid
 int run_macro(lbm_cuboid* h, double* rho, double* u, long long ustride, int zbeg, int n) {
   if (h->p.precision == LBM_FP64)
     lbm::k_macro<double><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], rho, u,
-                                                                        ustride, h->c, zbeg);
+                                                                        ustride, h->c, zbeg, aa_mode(h));
   else
     lbm::k_macro<float><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], rho, u,
-                                                                       ustride, h->c, zbeg);
+                                                                       ustride, h->c, zbeg, aa_mode(h));
   CU(cudaGetLastError());
   h->launches++;
   return LBM_OK;
@@ -453,6 +508,7 @@ int step_once(lbm_cuboid* h) {
   int rc;
   void* src = h->buf[h->cur];
   void* dst = h->buf[h->cur ^ 1];
+  if (h->aa) return launch_aa(h, h->stream);
   if (!h->ghost) {
     if (h->fd && (rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
     return launch_cs(h, src, dst, 0, h->nzl, 1, h->stream);
@@ -539,6 +595,7 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->peer_down = hp.peer_down;
   h->paper_rates = (p->omega_1 == 1.0 && p->omega_high == 1.0);
   h->fd = (p->corrections == LBM_CORR_FULL_FD);
+  h->aa = (p->streaming == LBM_STREAM_AA);
   fill_consts(h);
 
   auto bail = [&](int code) {
@@ -554,20 +611,23 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
     h->own_stream = true;
   }
   const size_t bytes = size_t(h->buf_elems) * h->elem;
+  const int nbuf = h->aa ? 1 : 2;  // AA streaming updates one buffer in place
   if (p->buf_a || p->buf_b) {
-    if (!p->buf_a || !p->buf_b) return bail(fail(LBM_EINVAL, "buf_a and buf_b must both be given or both NULL"));
+    if (!p->buf_a || (!h->aa && !p->buf_b))
+      return bail(fail(LBM_EINVAL, "buf_a and buf_b must both be given (buf_a only with AA) or both NULL"));
     h->buf[0] = p->buf_a;
-    h->buf[1] = p->buf_b;
+    h->buf[1] = h->aa ? p->buf_a : p->buf_b;
   } else {
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < nbuf; ++i)
       if (cudaMalloc(&h->buf[i], bytes) != cudaSuccess) {
         cudaGetLastError();
         return bail(fail(LBM_ENOMEM, "cudaMalloc(%zu) for a population buffer failed", bytes));
       }
+    if (h->aa) h->buf[1] = h->buf[0];
     h->own_buf = true;
   }
   // ghost planes must hold finite values even when unused (wall faces)
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < nbuf; ++i)
     if (cudaMemsetAsync(h->buf[i], 0, bytes, h->stream) != cudaSuccess)
       return bail(fail(LBM_ECUDA, "cudaMemsetAsync failed"));
   if (cudaMalloc(&h->d_check, 8 * sizeof(double)) != cudaSuccess) return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
@@ -605,6 +665,7 @@ int lbm_cuboid_init_fields_device(lbm_cuboid_t* h, const double* rho, const doub
   int rc = set_device(h);
   if (rc) return rc;
   if ((rc = wait_halo(h))) return rc;
+  if (h->aa) h->cur = 0;  // AA: the canonical state is written in layout R
   if ((rc = run_init(h, rho, u, (long long)h->nzl * h->nxy, 0, h->nzl))) return rc;
   return exchange(h, h->cur);
 }
@@ -614,6 +675,7 @@ int lbm_cuboid_init_fields(lbm_cuboid_t* h, const double* rho, const double* u) 
   int rc = set_device(h);
   if (rc) return rc;
   if ((rc = wait_halo(h))) return rc;
+  if (h->aa) h->cur = 0;  // AA: the canonical state is written in layout R
   const int cp = chunk_planes(h, 4);
   if ((rc = ensure_stage(h, size_t(4) * cp * h->nxy * sizeof(double)))) return rc;
   for (int z = 0; z < h->nzl; z += cp) {
@@ -709,10 +771,10 @@ int lbm_cuboid_get_populations_planes(lbm_cuboid_t* h, int32_t z_begin, int32_t 
     const size_t cnt = size_t(n) * h->nxy;
     if (h->p.precision == LBM_FP64)
       lbm::k_pack<double><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], h->stage, n,
-                                                                         h->c, z_begin + z);
+                                                                         h->c, z_begin + z, aa_mode(h));
     else
       lbm::k_pack<float><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], h->stage, n,
-                                                                        h->c, z_begin + z);
+                                                                        h->c, z_begin + z, aa_mode(h));
     CU(cudaGetLastError());
     h->launches++;
     CU(cudaMemcpy2DAsync(f + size_t(z) * h->nxy, size_t(n_planes) * h->nxy * 8, h->stage, cnt * 8, cnt * 8, 27,
@@ -732,6 +794,7 @@ int lbm_cuboid_set_populations(lbm_cuboid_t* h, const double* f) {
   int rc = set_device(h);
   if (rc) return rc;
   if ((rc = wait_halo(h))) return rc;
+  if (h->aa) h->cur = 0;  // AA: the canonical state is written in layout R
   const int cp = chunk_planes(h, 27);
   if ((rc = ensure_stage(h, size_t(27) * cp * h->nxy * sizeof(double)))) return rc;
   for (int z = 0; z < h->nzl; z += cp) {
@@ -741,10 +804,10 @@ int lbm_cuboid_set_populations(lbm_cuboid_t* h, const double* f) {
                          cudaMemcpyHostToDevice, h->stream));
     if (h->p.precision == LBM_FP64)
       lbm::k_unpack<double><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>(h->stage, (double*)h->buf[h->cur], n,
-                                                                           h->c, z);
+                                                                           h->c, z, h->aa ? 1 : 0);
     else
       lbm::k_unpack<float><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>(h->stage, (float*)h->buf[h->cur], n,
-                                                                          h->c, z);
+                                                                          h->c, z, h->aa ? 1 : 0);
     CU(cudaGetLastError());
     h->launches++;
     CU(cudaStreamSynchronize(h->stream));
@@ -759,9 +822,11 @@ int lbm_cuboid_check(lbm_cuboid_t* h, double out[7]) {
   CU(cudaMemsetAsync(h->d_check, 0, 8 * sizeof(double), h->stream));
   dim3 g = grid_for(h, h->nzl);
   if (h->p.precision == LBM_FP64)
-    lbm::k_check<double><<<g, lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], h->d_check, h->c);
+    lbm::k_check<double><<<g, lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], h->d_check, h->c,
+                                                           aa_mode(h));
   else
-    lbm::k_check<float><<<g, lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], h->d_check, h->c);
+    lbm::k_check<float><<<g, lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], h->d_check, h->c,
+                                                          aa_mode(h));
   CU(cudaGetLastError());
   h->launches++;
   CU(cudaMemcpyAsync(out, h->d_check, 7 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
@@ -845,7 +910,7 @@ int lbm_cuboid_destroy(lbm_cuboid_t* h) {
   if (h->ev_halo) cudaEventDestroy(h->ev_halo);
   if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
   if (h->own_buf)
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < (h->aa ? 1 : 2); ++i)
       if (h->buf[i]) cudaFree(h->buf[i]);
   if (h->stage) cudaFree(h->stage);
   if (h->d_check) cudaFree(h->d_check);

@@ -24,6 +24,7 @@ CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF, CORR_FULL_FD = 0, 1, 2, 3
 FP64, FP32_STORAGE = 0, 1
 HALO_AUTO, HALO_NCCL = 0, 1
 MODEL_CM, MODEL_RM = 0, 1
+STREAM_AB, STREAM_AA = 0, 1
 
 # every symbol include/lbm_cuboid.h declares
 EXPORTS = ["lbm_cuboid_default_params", "lbm_cuboid_buffer_bytes", "lbm_cuboid_halo_plan",
@@ -51,7 +52,7 @@ class Params(ctypes.Structure):
                 ("wall_u", ctypes.c_double), ("corrections", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("device", ctypes.c_int32), ("halo", ctypes.c_int32), ("graphs", ctypes.c_int32),
-                ("model", ctypes.c_int32),
+                ("model", ctypes.c_int32), ("streaming", ctypes.c_int32),
                 ("nccl_uid", ctypes.c_void_p), ("stream", ctypes.c_void_p),
                 ("buf_a", ctypes.c_void_p), ("buf_b", ctypes.c_void_p)]
 
@@ -115,7 +116,7 @@ def _check(rc):
 
 def make_params(nx, ny, nz, r, s, cs2=0.0, omega_nu=1.0, omega_xi=1.0, omega_1=1.0, omega_high=1.0,
                 force=(0.0, 0.0, 0.0), bc=(0,) * 6, wall_u=0.0, corrections=0, precision=0,
-                rank=0, world=1, device=0, halo=0, graphs=0, model=0) -> Params:
+                rank=0, world=1, device=0, halo=0, graphs=0, model=0, streaming=0) -> Params:
     p = Params()
     load().lbm_cuboid_default_params(ctypes.byref(p))
     p.nx, p.ny, p.nz = int(nx), int(ny), int(nz)
@@ -131,6 +132,7 @@ def make_params(nx, ny, nz, r, s, cs2=0.0, omega_nu=1.0, omega_xi=1.0, omega_1=1
     p.rank, p.world, p.device, p.halo = int(rank), int(world), int(device), int(halo)
     p.graphs = int(graphs)
     p.model = int(model)
+    p.streaming = int(streaming)
     return p
 
 
@@ -168,23 +170,25 @@ class Lattice:
 
     def __init__(self, nx, ny, nz, r, s, cs2=0.0, omega_nu=1.0, omega_xi=1.0, omega_1=1.0,
                  omega_high=1.0, force=(0.0, 0.0, 0.0), bc=(0,) * 6, wall_u=0.0, corrections=0,
-                 precision=0, rank=0, world=1, device=0, halo=0, graphs=0, model=0,
+                 precision=0, rank=0, world=1, device=0, halo=0, graphs=0, model=0, streaming=0,
                  nccl_uid: bytes | None = None, stream=None):
         import torch  # noqa: PLC0415  (device memory / streams only)
 
         L = load()
         self._torch = torch
         self.p = make_params(nx, ny, nz, r, s, cs2, omega_nu, omega_xi, omega_1, omega_high, force,
-                             bc, wall_u, corrections, precision, rank, world, device, halo, graphs, model)
+                             bc, wall_u, corrections, precision, rank, world, device, halo, graphs, model,
+                             streaming)
         self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
         self.world, self.rank = int(world), int(rank)
         self.nzl = self.nz // self.world
         self.r, self.s = float(r), float(s)
         self.device = torch.device("cuda", int(device))
         nbytes = buffer_bytes(self.p)
-        self._bufs = [torch.empty(nbytes, dtype=torch.uint8, device=self.device) for _ in range(2)]
+        nbuf = 1 if int(streaming) == STREAM_AA else 2
+        self._bufs = [torch.empty(nbytes, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
         self.p.buf_a = self._bufs[0].data_ptr()
-        self.p.buf_b = self._bufs[1].data_ptr()
+        self.p.buf_b = self._bufs[1].data_ptr() if nbuf == 2 else None
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
             if stream.cuda_stream == 0:

@@ -21,13 +21,18 @@ cases = [
     synth.CONFIGS["shear"].scaled(nx=8, ny=12, nz=6),
     synth.CONFIGS["duct"].scaled(nx=3, ny=10, nz=7),
     synth.Workload("generic", 9, 7, 5, r=0.75, s=1.3, nu=0.02, omega_1=1.2, omega_high=0.9, init="random"),
+    synth.CONFIGS["tgv"].scaled(nx=7, ny=6, nz=5, corrections=synth.CORR_FULL_FD),
+    synth.CONFIGS["cavity100"].scaled(nx=6, ny=7, nz=4, corrections=synth.CORR_FULL_FD),
 ]
 for w in cases:
     for prec in (0, 1):
         for model in (0, 1):
             ww = w.scaled(precision=prec, model=model)
-            for kw in ({}, {"halo": 1, "nccl_uid": P.nccl_unique_id()}, {"graphs": 2}):
+            for kw in ({}, {"halo": 1, "nccl_uid": P.nccl_unique_id()}, {"graphs": 2}, {"streaming": 1},
+                       {"streaming": 1, "graphs": 2}):
                 if "halo" in kw and ww.bc[4] != 0:
+                    continue
+                if "streaming" in kw and ww.corrections == synth.CORR_FULL_FD:
                     continue
                 g = P.Lattice(**ww.params(), **kw)
                 rho, u = synth.random_fields(ww.nx, ww.ny, ww.nz, 5)

@@ -18,8 +18,10 @@ def test_bounds_checked_kernels():
 
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
+    from paper_2107_14774_b200 import build as B
+
     lib = os.path.join(ROOT, "build", "variants", "lib_debug.so")
-    if not os.path.exists(lib):
+    if not os.path.exists(lib) or any(os.path.getmtime(s) > os.path.getmtime(lib) for s in B.sources()):
         subprocess.check_call([sys.executable, os.path.join(ROOT, "scripts", "sweep.py"), "build", "debug"])
     env = dict(os.environ, LBM_CUBOID_LIB=lib)
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "sanitize_run.py")], env=env,

@@ -456,3 +456,77 @@ def test_full_size_config3_cavity_properties(P):
     assert np.abs(uu[0] - mir[0]).max() < 1e-9 * scale
     assert np.abs(uu[1] - mir[1]).max() < 1e-9 * scale
     assert np.abs(uu[2] + mir[2]).max() < 1e-9 * scale
+
+
+# ----------------------------------------------------- AA in-place streaming
+def _run_ab_aa(P, w, steps, seed=61, **kw):
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, seed)
+    a = _gpu(P, w, **kw)
+    b = _gpu(P, w, streaming=P.STREAM_AA, **kw)
+    a.init_fields(rho, u)
+    b.init_fields(rho, u)
+    a.step(steps)
+    b.step(steps)
+    return a, b
+
+
+@pytest.mark.parametrize("steps", [1, 2, 37, 64])
+@pytest.mark.parametrize("name", ["weak_tgv", "duct", "shear"])
+def test_aa_equals_ab_bitwise(P, name, steps):
+    """AA in-place streaming (one buffer) reproduces the two-buffer scheme bit for
+    bit (same per-node arithmetic, same values gathered) after odd and even step
+    counts, with periodic, bounce-back and free-slip faces."""
+    w = CASES[name]
+    a, b = _run_ab_aa(P, w, steps)
+    fa, fb = a.get_populations(), b.get_populations()
+    assert np.array_equal(fa, fb)
+    ra, ua = a.get_macroscopic()
+    rb, ub = b.get_macroscopic()
+    assert np.array_equal(ra, rb) and np.array_equal(ua, ub)
+    assert a.check()["mass"] == pytest.approx(b.check()["mass"], rel=1e-15)
+
+
+@pytest.mark.parametrize("model", [0, 1])
+@pytest.mark.parametrize("steps", [1, 30, 31])
+def test_aa_lid_cavity_and_models(P, model, steps):
+    """Moving lid (the push uses rho_f = rho of the node, equal to sum f~ up to
+    rounding): AA vs AB within 1e-14, and AA vs the oracle within the parity bar."""
+    w = CASES["cavity100"].scaled(model=model)
+    a, b = _run_ab_aa(P, w, steps)
+    assert np.abs(a.get_populations() - b.get_populations()).max() < 1e-14
+    o, _ = _init_both(P, w, seed=61)
+    o.step(steps)
+    _cmp(o, b)
+
+
+def test_aa_fp32_generic_rates_graphs_and_set_populations(P):
+    w = synth.Workload("aa-generic", 13, 11, 9, r=0.75, s=1.3, nu=0.02, omega_xi=1.3, omega_1=1.2,
+                       omega_high=0.9, force=(1e-5, 0.0, -2e-5), bc=(0, 0, 1, 2, 0, 0), wall_u=0.03,
+                       init="random", seed=4)
+    for prec in (0, 1):
+        ww = w.scaled(precision=prec)
+        a, b = _run_ab_aa(P, ww, 45, seed=4)
+        d = np.abs(a.get_populations() - b.get_populations()).max()
+        assert d < (1e-14 if prec == 0 else 1e-6), d
+    # graphs (32-step replays) and a set_populations restart in layout R
+    ww = w.scaled(nx=21, ny=19, nz=11)
+    a, b = _run_ab_aa(P, ww, 70, seed=5, graphs=2)
+    c = _gpu(P, ww, streaming=P.STREAM_AA, graphs=1)
+    rho, u = synth.random_fields(ww.nx, ww.ny, ww.nz, 5)
+    c.init_fields(rho, u)
+    c.step(70)
+    assert np.array_equal(b.get_populations(), c.get_populations())
+    f = b.get_populations()
+    b.set_populations(f)
+    a.set_populations(f)
+    a.step(9)
+    b.step(9)
+    assert np.abs(a.get_populations() - b.get_populations()).max() < 1e-14
+
+
+def test_aa_rejects_multi_gpu_and_fd(P):
+    w = CASES["weak_tgv"]
+    with pytest.raises(P.LbmError):
+        _gpu(P, w, streaming=P.STREAM_AA, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id())
+    with pytest.raises(P.LbmError):
+        _gpu(P, w.scaled(corrections=synth.CORR_FULL_FD), streaming=P.STREAM_AA)
