@@ -15,7 +15,6 @@ populations.  Layouts: scalar fields are C-ordered [z][y][x]; vector fields are
 from __future__ import annotations
 
 import dataclasses
-import math
 
 import numpy as np
 
@@ -210,4 +209,4 @@ def reynolds(w: Workload, length: float, speed: float) -> float:
     return speed * length / w.nu
 
 
-__all__ = [n for n in dir() if not n.startswith("_") and n not in ("math", "np", "dataclasses")]
+__all__ = [n for n in dir() if not n.startswith("_") and n not in ("np", "dataclasses", "annotations")]
