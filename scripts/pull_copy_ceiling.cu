@@ -31,6 +31,29 @@ __global__ void __launch_bounds__(128) pull_copy(const double* __restrict__ src,
   for (int q = 0; q < 27; ++q) __stcs(out + q * nxy, f[q]);
 }
 
+// plain vectorized copy of the same number of bytes (16-B loads/stores)
+__global__ void __launch_bounds__(256) plain_copy(const double2* __restrict__ src, double2* __restrict__ dst, size_t n) {
+  size_t i = blockIdx.x * (size_t)256 + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * 256;
+  for (; i < n; i += stride) __stcs(dst + i, __ldg(src + i));
+}
+
+// 27 aligned streams (no shifts), same structure as the pull copy
+__global__ void __launch_bounds__(128) aligned27(const double* __restrict__ src, double* __restrict__ dst, int nx,
+                                                 int ny) {
+  const int nxy = nx * ny;
+  const int idx = blockIdx.x * 128 + threadIdx.x;
+  if (idx >= nxy) return;
+  const long long plane = 27LL * nxy;
+  const double* in = src + (blockIdx.y + 1) * plane + idx;
+  double f[27];
+#pragma unroll
+  for (int q = 0; q < 27; ++q) f[q] = __ldg(in + q * nxy);
+  double* out = dst + (blockIdx.y + 1) * plane + idx;
+#pragma unroll
+  for (int q = 0; q < 27; ++q) __stcs(out + q * nxy, f[q]);
+}
+
 int main() {
   const int nx = 512, ny = 512, nz = 512;
   const size_t elems = 27ull * nx * ny * (nz + 2);
@@ -51,6 +74,29 @@ int main() {
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const double nodes = double(nx) * ny * nz;
+  {
+    const size_t n2 = size_t(27) * nx * ny * nz / 2;
+    cudaEvent_t a0, a1;
+    cudaEventCreate(&a0);
+    cudaEventCreate(&a1);
+    for (int w = 0; w < 2; ++w) plain_copy<<<148 * 16, 256>>>((const double2*)a, (double2*)b, n2);
+    cudaEventRecord(a0);
+    for (int t = 0; t < 20; ++t) plain_copy<<<148 * 16, 256>>>((const double2*)((t & 1) ? b : a), (double2*)((t & 1) ? a : b), n2);
+    cudaEventRecord(a1);
+    cudaEventSynchronize(a1);
+    float m2 = 0;
+    cudaEventElapsedTime(&m2, a0, a1);
+    printf("{\"kernel\": \"plain 16B copy, same bytes\", \"ms\": %.4f, \"GBps\": %.1f}\n", m2 / 20,
+           432.0 * nodes * 20 / (m2 * 1e-3) / 1e9);
+    for (int w = 0; w < 2; ++w) aligned27<<<g, 128>>>(a, b, nx, ny);
+    cudaEventRecord(a0);
+    for (int t = 0; t < 20; ++t) aligned27<<<g, 128>>>((t & 1) ? b : a, (t & 1) ? a : b, nx, ny);
+    cudaEventRecord(a1);
+    cudaEventSynchronize(a1);
+    cudaEventElapsedTime(&m2, a0, a1);
+    printf("{\"kernel\": \"27 aligned streams, no shift\", \"ms\": %.4f, \"GBps\": %.1f}\n", m2 / 20,
+           432.0 * nodes * 20 / (m2 * 1e-3) / 1e9);
+  }
   printf("{\"kernel\": \"pull_copy (no arithmetic)\", \"ms_per_step\": %.4f, \"mlups\": %.1f, \"GBps_432B\": %.1f, \"err\": \"%s\"}\n",
          ms / n, nodes * n / (ms * 1e-3) / 1e6, 432.0 * nodes * n / (ms * 1e-3) / 1e9,
          cudaGetErrorString(cudaGetLastError()));
