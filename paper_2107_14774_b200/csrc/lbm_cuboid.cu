@@ -333,6 +333,7 @@ int launch_density(lbm_cuboid* h, const void* src, int zbeg, int nplanes, int zs
 }
 
 void drop_graphs(lbm_cuboid* h) {
+  if (h->gexec[0] || h->gexec[1]) cudaStreamSynchronize(h->stream);  // a replay may still be running
   for (auto& g : h->gexec)
     if (g) {
       cudaGraphExecDestroy(g);
