@@ -31,10 +31,15 @@
  * (rho_f of Eq. 69 at the wall-adjacent node, same time level as the reflected
  * f~), R5 (lid augmentation on every link whose source crosses the +y face),
  * R6 (a wall wins over periodicity), R7 (free-slip = halfway specular
- * reflection), R8 (init f~ = f^eq(rho0, u0 + F/(2 rho0))).
+ * reflection), R8 (init f~ = f^eq(rho0, u0 + F/(2 rho0))), R16 (FULL_FD: the
+ * isotropic lattice gradient of the same-time density).
  *
  * Parity pins: tests/test_oracle_*.py (closed forms, paper-printed appendices
- * and Eq. 69, conservation, SRT limit, analytic TGV/shear-wave/duct decay).
+ * and Eq. 69, conservation, SRT limit, analytic TGV/shear-wave/duct decay,
+ * viscous and acoustic isotropy, Galilean invariance, moving-frame sound
+ * attenuation for the density-gradient terms, Womersley).
+ * Parity unpinned: the free-slip rule (reading R7) is not in the paper; it is
+ * checked only against invariants (mass and tangential momentum conservation).
  *
  * Population layout of every array argument: [q][z][y][x], q in the paper's
  * order of Eqs. 1a-1c, x fastest.
