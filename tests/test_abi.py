@@ -92,3 +92,13 @@ def test_halo_plan(P, world, bcz):
     p = P.lbm.make_params(nx, ny, nz, 1.0, 2.0, omega_nu=1.5, halo=1)
     hp = P.lbm.halo_plan(p)
     assert hp["ghost"] == 1 and hp["peer_up"] == 0 and hp["peer_down"] == 0
+
+
+def test_c_example_compiles_against_the_header(P, tmp_path):
+    """examples/tgv_c_abi.c uses only include/lbm_cuboid.h and the shared library."""
+    exe = tmp_path / "tgv_c_abi"
+    subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "tgv_c_abi.c"), "-o", str(exe),
+                           "-L", os.path.dirname(P.lbm.LIB_PATH), "-l:liblbm_cuboid.so",
+                           f"-Wl,-rpath,{os.path.dirname(P.lbm.LIB_PATH)}", "-lm"])
+    assert exe.exists()

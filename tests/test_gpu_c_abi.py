@@ -1,0 +1,41 @@
+"""The plain-C program examples/tgv_c_abi.c (no Python, no torch) drives the
+library through the C ABI; its result equals the Python binding's (the C side
+computes its initial fields with libm, so they may differ in the last ulp).""" 
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_c_program_matches_python_binding(tmp_path):
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2107_14774_b200 as P
+
+    libdir = os.path.dirname(P.lbm.LIB_PATH)
+    exe = tmp_path / "tgv_c_abi"
+    subprocess.check_call(["gcc", "-O2", "-std=c99", "-I", os.path.join(ROOT, "include"),
+                           os.path.join(ROOT, "examples", "tgv_c_abi.c"), "-o", str(exe), "-L", libdir,
+                           "-l:liblbm_cuboid.so", f"-Wl,-rpath,{libdir}", "-lm"])
+    out = tmp_path / "out.bin"
+    r = subprocess.run([str(exe), "200", str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    w = synth.CONFIGS["tgv"]
+    g = P.Lattice(**w.params())
+    rho, u = synth.initial_fields(w)
+    g.init_fields(rho, u)
+    g.step(200)
+    rp, up = g.get_macroscopic()
+    data = np.fromfile(out, dtype=np.float64)
+    n = w.nodes
+    assert np.abs(data[:n].reshape(rp.shape) - rp).max() < 1e-13
+    assert np.abs(data[n:].reshape(up.shape) - up).max() < 1e-13
+    assert '"mass_change"' in r.stdout
