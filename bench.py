@@ -50,9 +50,11 @@ def parse():
     ap.add_argument("--nz-per-gpu", type=int, default=None, help="override the per-GPU slab depth")
     ap.add_argument("--corrections", choices=["full_local", "low_mach", "off", "full_fd"], default="full_local")
     ap.add_argument("--model", choices=["cm", "rm"], default="cm")
-    ap.add_argument("--halo", choices=["auto", "nccl"], default="auto",
+    ap.add_argument("--halo", choices=["auto", "nccl", "p2p"], default="auto",
                     help="nccl: force the multi-GPU step structure (boundary launch, NCCL ghost-plane "
-                         "exchange on the comm stream, interior launch) even on one GPU (send to self)")
+                         "exchange on the comm stream, interior launch) even on one GPU (send to self); "
+                         "p2p: fused halo (the boundary-plane kernel stores into the neighbours' ghost "
+                         "planes over peer memory, concurrent with the interior; on one GPU into its own)")
     return ap.parse_args()
 
 
@@ -224,6 +226,8 @@ def run_cuda(args):
     kw = w.params()
     if args.streaming == "aa":
         kw["streaming"] = P.STREAM_AA
+    if args.halo == "p2p":
+        kw["halo"] = P.HALO_P2P
     if world > 1:
         lat = P.distributed_lattice(device=local, **kw)
     elif args.halo == "nccl":
@@ -342,7 +346,8 @@ def run_cuda(args):
             "launches_timed": tk["launches"],
             "note": "achieved = 2*27*sizeof(real) B/node x nodes per launch / mean launch duration (library "
                     "CUDA events around each collide-stream launch on the compute stream, K steps after the "
-                    "timed region; at N>1 a step has 2 launches: boundary planes + interior)"}
+                    "timed region; at N>1 a step has 2 launches: boundary planes + interior; with the fused P2P halo "
+                    "one event pair spans both concurrent launches of a step)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         v, n, ws = oracle_mlups(w, budget_s=12.0)
@@ -357,7 +362,7 @@ def run_cuda(args):
                        "model": "3DCCM" if w.model == 0 else "3DCRM", "storage": prec,
                        "l2": "working set per step >> 126 MB L2; no flush needed",
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
-                       "halo": "nccl ghost planes" if lat.info()["nccl_halo"] else "in-kernel wrap",
+                       "halo": {0: "in-kernel wrap", 1: "nccl ghost planes", 2: "fused p2p ghost planes"}[lat.info()["halo"]],
                        "streaming": "AA in place (1 buffer)" if args.streaming == "aa" else "AB (2 buffers)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "bad_nodes": bad}

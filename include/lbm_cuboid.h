@@ -91,8 +91,18 @@ typedef enum {
 
 typedef enum {
   LBM_HALO_AUTO = 0, /* 1 GPU + periodic z: wrap inside the kernel; else NCCL ghost planes */
-  LBM_HALO_NCCL = 1  /* always exchange ghost planes with NCCL (also world == 1: send to self) */
+  LBM_HALO_NCCL = 1, /* always exchange ghost planes with NCCL (also world == 1: send to self) */
+  LBM_HALO_P2P = 2   /* fused halo: the boundary-plane collide-stream kernel stores the outgoing
+                        directions straight into the neighbours' ghost planes (peer memory over
+                        NVLink; CUDA IPC between processes, direct pointers within one process)
+                        and publishes a per-step epoch flag; the neighbour's stream waits on the
+                        flag (no NCCL, no spinning kernel).  The boundary planes run on a second,
+                        high-priority stream concurrently with the interior.  Requires
+                        lbm_cuboid_p2p_connect() when world > 1; not with LBM_CORR_FULL_FD or AA. */
 } lbm_halo;
+
+/* Size of the opaque blob lbm_cuboid_p2p_export() writes. */
+#define LBM_P2P_BLOB_BYTES 512
 
 typedef struct {
   int32_t nx, ny, nz;          /* GLOBAL node counts (>= 1); nz % world == 0 */
@@ -135,16 +145,34 @@ int lbm_cuboid_buffer_bytes(const lbm_cuboid_params *p, int64_t *bytes);
 
 /* Host-only halo plan of this rank (no GPU needed), element offsets into one
  * population buffer (layout: DESIGN.md "Data layout"):
- * out[0] = 1 if ghost planes are exchanged (world > 1 or LBM_HALO_NCCL),
+ * out[0] = 1 if ghost planes are exchanged (world > 1, or periodic z with
+ *          LBM_HALO_NCCL / LBM_HALO_P2P),
  * out[1] = peer above (-1 none), out[2] = peer below (-1 none),
  * out[3] = elements per message (9 * nx * ny),
  * out[4] = send-up offset (top plane, the 9 directions with e_z = +1),
  * out[5] = recv-down offset (lower ghost plane, e_z = +1 directions),
  * out[6] = send-down offset (bottom plane, e_z = -1 directions),
  * out[7] = recv-up offset (upper ghost plane, e_z = -1 directions).
- * Every rank issues, inside one NCCL group: send(up), recv(down), send(down),
- * recv(up), skipping absent peers. */
+ * NCCL: every rank issues, inside one NCCL group: send(up), recv(down),
+ * send(down), recv(up), skipping absent peers.  P2P: the send regions are
+ * stored by the boundary kernel at the neighbours' recv offsets. */
 int lbm_cuboid_halo_plan(const lbm_cuboid_params *p, int64_t out[8]);
+
+/* LBM_HALO_P2P wiring.  export: write this handle's LBM_P2P_BLOB_BYTES-byte
+ * descriptor (IPC handles and addresses of both population buffers and of the
+ * flag words, pid, geometry) into blob.  connect: map the neighbours' buffers
+ * (blob_down = the rank below, blob_up = the rank above, as given by
+ * lbm_cuboid_halo_plan; NULL where there is no neighbour; the same blob twice
+ * when both neighbours are one rank).  Every rank calls connect once, after
+ * all ranks have created their handles and before init_fields / step; with
+ * world == 1 create() connects the handle to itself.  Errors: LBM_EINVAL for
+ * a blob of another geometry/precision or a missing neighbour, LBM_ECUDA if
+ * the peer mapping fails.  Handles of one process (e.g. several ranks' slabs
+ * driven from one thread) are connected with direct pointers.  The neighbours
+ * must stay alive until this handle is destroyed (destroy waits, up to 30 s,
+ * for the neighbours' last epoch so no peer store is in flight). */
+int lbm_cuboid_p2p_export(const lbm_cuboid_t *h, void *blob);
+int lbm_cuboid_p2p_connect(lbm_cuboid_t *h, const void *blob_down, const void *blob_up);
 
 /* Write a fresh 128-byte ncclUniqueId into out (call on rank 0 only). */
 int lbm_cuboid_nccl_unique_id(void *out128);
@@ -198,7 +226,7 @@ int lbm_cuboid_set_force(lbm_cuboid_t *h, const double force[3]);
  * out[1] = collide-stream launches, out[2] = steps taken,
  * out[3] = algorithmic bytes per node update (2 * 27 * sizeof(real)),
  * out[4] = local node count, out[5] = bytes of one buffer,
- * out[6] = 1 if NCCL ghost exchange is active,
+ * out[6] = ghost-plane exchange: 0 none (in-kernel wrap), 1 NCCL, 2 fused P2P,
  * out[7] = 1 if the paper-rate specialisation (omega_1 = omega_high = 1) is used. */
 int lbm_cuboid_info(const lbm_cuboid_t *h, int64_t out[8]);
 

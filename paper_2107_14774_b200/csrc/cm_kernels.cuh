@@ -858,6 +858,108 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T*
   collide_stream_ab<T, CORE_RAW, FD>(src, dst, rf, c, zbeg, zstride);
 }
 
+// ------------------------------------ fused collide-stream + peer-memory halo (P2P)
+// LBM_HALO_P2P: the launch over the two boundary planes of the slab also stores
+// the nine outgoing directions of each boundary plane straight into the
+// neighbour's ghost plane of the same time level (NVLink peer memory, or this
+// GPU's own ghost plane when the neighbour is this slab), then the last CTA
+// publishes the step's epoch in the neighbours' flag words.  A neighbour's
+// stream waits for that epoch (cuStreamWaitValue32) before its next boundary
+// launch, so no kernel ever spins on another rank.
+template <typename T>
+struct P2PArgs {
+  T* up;                 // up neighbour's buffer of this time level (nullptr: none)
+  T* dn;                 // down neighbour's buffer of this time level (nullptr: none)
+  unsigned int* counter; // CTA arrival counter (own device memory, 0 between launches)
+  unsigned int* flag_up; // my slot in the up neighbour's flag words (nullptr: none)
+  unsigned int* flag_dn; // my slot in the down neighbour's flag words
+  unsigned int epoch;    // value published when every CTA has stored
+};
+
+// Own-node store plus the peer copy of the outgoing directions:
+//   top plane (z = nz_l - 1), e_z = +1 (q 18..26) -> up neighbour's ghost p = 0
+//   bottom plane (z = 0),     e_z = -1 (q 0..8)   -> down neighbour's ghost p = nz_l + 1
+// (the pull of the neighbour's plane adjacent to the ghost reads exactly these).
+template <typename T>
+struct StoreHalo {
+  T* base;
+  T* out;
+  int nxy;
+  const Consts* c;
+  T* rup;  // up neighbour's ghost plane at this node, or nullptr
+  T* rdn;  // down neighbour's ghost plane at this node, or nullptr
+  const T* up_base;
+  const T* dn_base;
+  __device__ __forceinline__ void begin(double) {}
+  __device__ __forceinline__ void operator()(int q, double v) const {
+    stcs<T>(LBM_CHECK_ST(base, out + q * nxy, *c), v);
+    if (q >= 18 && rup) stcs<T>(LBM_CHECK_ST(up_base, rup + q * nxy, *c), v);
+    if (q < 9 && rdn) stcs<T>(LBM_CHECK_ST(dn_base, rdn + q * nxy, *c), v);
+  }
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Every CTA: barrier, system fence (its peer stores are visible system-wide
+// before it arrives), arrive.  The last CTA to arrive resets the counter and
+// publishes the epoch (fence-cumulative: all CTAs' stores precede the flag).
+template <typename T>
+__device__ __forceinline__ void p2p_signal(const P2PArgs<T>& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    const unsigned int total = gridDim.x * gridDim.y;
+    if (atomicAdd(a.counter, 1u) == total - 1) {
+      atomicExch(a.counter, 0u);
+      __threadfence_system();
+      if (a.flag_up) st_release_sys(a.flag_up, a.epoch);
+      if (a.flag_dn) st_release_sys(a.flag_dn, a.epoch);
+    }
+  }
+}
+
+template <typename T, int KIND>
+__global__ void LBM_CS_BOUNDS k_collide_stream_p2p(const T* __restrict__ src, T* __restrict__ dst,
+                                                   const __grid_constant__ Consts c, int zbeg, int zstride,
+                                                   const P2PArgs<T> a) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx < c.nxy) {  // no early return: every thread reaches the barrier of p2p_signal
+    const int y = idx / c.nx;
+    const int x = idx - y * c.nx;
+    const int z = zbeg + blockIdx.y * zstride;
+    double f[27];
+    gather<T>(src, c, x, y, z, f);
+    StoreHalo<T> st{dst,
+                    dst + (long long)(z + 1) * c.plane + idx,
+                    c.nxy,
+                    &c,
+                    (z == c.nzl - 1 && a.up) ? a.up + idx : nullptr,
+                    (z == 0 && a.dn) ? a.dn + (long long)(c.nzl + 1) * c.plane + idx : nullptr,
+                    a.up,
+                    a.dn};
+    run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, st);
+  }
+  p2p_signal(a);
+}
+
+// Halo publish without a collision (after init_fields / set_populations): copy
+// the outgoing directions of the two boundary planes of `src` into the
+// neighbours' ghost planes (blockIdx.y = 0: down, 1: up), then signal.
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_halo_push(const T* __restrict__ src, const __grid_constant__ Consts c,
+                                                      const P2PArgs<T> a) {
+  const long long e = (long long)blockIdx.x * kBlock + threadIdx.x;
+  if (e < 9LL * c.nxy) {
+    if (blockIdx.y == 0 && a.dn)  // bottom plane p = 1, q 0..8 -> ghost p = nz_l + 1
+      a.dn[(long long)(c.nzl + 1) * c.plane + e] = src[c.plane + e];
+    if (blockIdx.y == 1 && a.up)  // top plane p = nz_l, q 18..26 -> ghost p = 0
+      a.up[18LL * c.nxy + e] = src[(long long)c.nzl * c.plane + 18LL * c.nxy + e];
+  }
+  p2p_signal(a);
+}
+
 // ------------------------------------------------ AA in-place streaming (one buffer)
 // Layout R: slot 26 - q of node x holds f~_q(x) (post-collision, canonical);
 // layout N: slot q of node x holds f_q(x) (pre-collision, already streamed).

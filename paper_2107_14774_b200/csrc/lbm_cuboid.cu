@@ -10,18 +10,27 @@
 //                     the two boundary planes into the neighbours' ghost planes
 //                     -> record(halo[t])
 //     compute stream: interior planes 1..nz_l-2 (overlaps the exchange)
+//   fused P2P halo (LBM_HALO_P2P):
+//     halo stream   : wait(compute) -> wait(neighbours' epoch flags >= e) ->
+//                     boundary planes, storing the outgoing directions into the
+//                     neighbours' ghost planes and publishing epoch e + 1
+//     compute stream: interior planes 1..nz_l-2 (concurrent) -> wait(halo stream)
 #include "../../include/lbm_cuboid.h"
 #include "cm_kernels.cuh"
 
+#include <cuda.h>  // driver types only; entry points come from cudaGetDriverEntryPointByVersion
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 using lbm::Consts;
@@ -81,6 +90,16 @@ struct lbm_cuboid {
   cudaEvent_t ev_rho = nullptr;
   ncclComm_t comm = nullptr;
   int peer_down = -1, peer_up = -1;  // ranks owning the planes below / above, -1 none
+  // fused P2P halo (LBM_HALO_P2P); comm_stream is the (high-priority) halo stream
+  bool p2p = false, p2p_ready = false;
+  unsigned int* d_sig = nullptr;  // [0] epoch from the down neighbour, [1] from the up one, [2] CTA counter
+  void* peer_buf_up[2] = {nullptr, nullptr};  // neighbours' population buffers, mapped
+  void* peer_buf_dn[2] = {nullptr, nullptr};
+  unsigned int* peer_flag_up = nullptr;  // my slot in the up neighbour's flag words ([0])
+  unsigned int* peer_flag_dn = nullptr;  // my slot in the down neighbour's flag words ([1])
+  std::vector<void*> ipc_open;           // IPC mappings to close
+  uint32_t epoch = 0;                    // halo publishes enqueued so far
+  cudaEvent_t ev_fork = nullptr;
   Consts c{};
   double* stage = nullptr;
   size_t stage_bytes = 0;
@@ -127,12 +146,14 @@ int validate(const lbm_cuboid_params* p) {
       return fail(LBM_EINVAL, "configuration error: a moving wall is supported on the +y face only (P:L751)");
   if (p->corrections < 0 || p->corrections > 3) return fail(LBM_EINVAL, "corrections must be an lbm_corr");
   if (p->precision < 0 || p->precision > 1) return fail(LBM_EINVAL, "precision must be an lbm_prec");
-  if (p->halo < 0 || p->halo > 1) return fail(LBM_EINVAL, "halo must be an lbm_halo");
+  if (p->halo < 0 || p->halo > 2) return fail(LBM_EINVAL, "halo must be an lbm_halo");
+  if (p->halo == LBM_HALO_P2P && p->corrections == LBM_CORR_FULL_FD)
+    return fail(LBM_ENOTSUP, "LBM_HALO_P2P does not support FULL_FD (use LBM_HALO_NCCL)");
   if (p->graphs < 0 || p->graphs > 2) return fail(LBM_EINVAL, "graphs must be 0, 1 or 2");
   if (p->model < 0 || p->model > 1) return fail(LBM_EINVAL, "model must be an lbm_model");
   if (p->streaming < 0 || p->streaming > 1) return fail(LBM_EINVAL, "streaming must be an lbm_streaming");
   if (p->streaming == LBM_STREAM_AA) {
-    if (p->world > 1 || p->halo == LBM_HALO_NCCL)
+    if (p->world > 1 || p->halo != LBM_HALO_AUTO)
       return fail(LBM_ENOTSUP, "AA in-place streaming is single-GPU only (no ghost-plane exchange)");
     if (p->corrections == LBM_CORR_FULL_FD)
       return fail(LBM_ENOTSUP, "AA in-place streaming does not support FULL_FD");
@@ -223,11 +244,28 @@ dim3 grid_for(const lbm_cuboid* h, int nplanes) {
   return dim3(unsigned((h->nxy + lbm::kBlock - 1) / lbm::kBlock), unsigned(nplanes), 1);
 }
 
-int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, int zstride, cudaStream_t s) {
+// P2P halo arguments of a boundary launch / halo push into the neighbours'
+// buffer `which`, publishing `epoch`
+template <typename T>
+lbm::P2PArgs<T> p2p_args(const lbm_cuboid* h, int which, uint32_t epoch) {
+  lbm::P2PArgs<T> a;
+  a.up = (T*)h->peer_buf_up[which];
+  a.dn = (T*)h->peer_buf_dn[which];
+  a.counter = h->d_sig + 2;
+  a.flag_up = h->peer_flag_up;
+  a.flag_dn = h->peer_flag_dn;
+  a.epoch = epoch;
+  return a;
+}
+
+// p2p_which >= 0: fused P2P boundary launch storing into the neighbours' buffer
+// p2p_which and publishing p2p_epoch (LBM_HALO_P2P)
+int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, int zstride, cudaStream_t s,
+              int p2p_which = -1, uint32_t p2p_epoch = 0, bool allow_timing = true) {
   if (nplanes <= 0) return LBM_OK;
   dim3 g = grid_for(h, nplanes);
   const bool fp64 = (h->p.precision == LBM_FP64);
-  const bool timed = h->timing && h->ev_t.size() < kMaxTimedLaunches;
+  const bool timed = allow_timing && h->timing && h->ev_t.size() < kMaxTimedLaunches;
   if (timed) {
     cudaEvent_t a, b;
     CU(cudaEventCreate(&a));
@@ -254,13 +292,32 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
                                                              zstride);                                       \
     }                                                                                                        \
   } while (0)
-  if (h->p.model == LBM_MODEL_RM)
+#define LBM_P2P(T)                                                                                           \
+  do {                                                                                                       \
+    const lbm::P2PArgs<T> a = p2p_args<T>(h, p2p_which, p2p_epoch);                                          \
+    if (h->p.model == LBM_MODEL_RM)                                                                          \
+      lbm::k_collide_stream_p2p<T, lbm::CORE_RAW><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, h->c, zbeg, \
+                                                                            zstride, a);                     \
+    else if (h->paper_rates)                                                                                 \
+      lbm::k_collide_stream_p2p<T, lbm::CORE_PAPER><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, h->c,  \
+                                                                              zbeg, zstride, a);             \
+    else                                                                                                     \
+      lbm::k_collide_stream_p2p<T, lbm::CORE_GENERIC><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, h->c, \
+                                                                                zbeg, zstride, a);           \
+  } while (0)
+  if (p2p_which >= 0) {
+    if (fp64)
+      LBM_P2P(double);
+    else
+      LBM_P2P(float);
+  } else if (h->p.model == LBM_MODEL_RM)
     LBM_LAUNCH(k_collide_stream_raw);
   else if (h->paper_rates)
     LBM_LAUNCH(k_collide_stream_paper);
   else
     LBM_LAUNCH(k_collide_stream);
 #undef LBM_LAUNCH
+#undef LBM_P2P
   CU(cudaGetLastError());
   if (timed) {
     CU(cudaEventRecord(h->ev_t.back().second, s));
@@ -387,7 +444,7 @@ struct HaloPlan {
 HaloPlan make_plan(const lbm_cuboid_params* p) {
   HaloPlan hp{};
   const bool zper = (p->bc[4] == LBM_BC_PERIODIC);
-  hp.ghost = (p->world > 1) || (p->halo == LBM_HALO_NCCL && zper);
+  hp.ghost = (p->world > 1) || (p->halo != LBM_HALO_AUTO && zper);
   hp.peer_up = hp.peer_down = -1;
   if (hp.ghost) {
     hp.peer_up = (p->rank < p->world - 1 || zper) ? (p->rank + 1) % p->world : -1;
@@ -403,10 +460,13 @@ HaloPlan make_plan(const lbm_cuboid_params* p) {
   return hp;
 }
 
+int p2p_push(lbm_cuboid* h, int which);
+
 // NCCL exchange of buffer `which`'s boundary planes into the neighbours' ghost
 // planes, on the comm stream, after the work already enqueued on the compute stream.
 int exchange(lbm_cuboid* h, int which) {
   if (!h->ghost) return LBM_OK;
+  if (h->p2p) return p2p_push(h, which);
   CU(cudaEventRecord(h->ev_bnd, h->stream));
   CU(cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
   const HaloPlan hp = make_plan(&h->p);
@@ -452,6 +512,120 @@ int wait_halo(lbm_cuboid* h) {
   if (h->halo_pending) {
     CU(cudaStreamWaitEvent(h->stream, h->ev_halo, 0));
     h->halo_pending = false;
+  }
+  return LBM_OK;
+}
+
+// ------------------------------------------------------- fused P2P halo (LBM_HALO_P2P)
+typedef CUresult (*PfnWaitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PfnAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+template <typename F>
+int driver_fn(const char* name, F* out) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q = cudaDriverEntryPointSymbolNotFound;
+  CU(cudaGetDriverEntryPointByVersion(name, &fn, 12000, cudaEnableDefault, &q));
+  if (q != cudaDriverEntryPointSuccess || !fn) return fail(LBM_ECUDA, "driver entry point %s is unavailable", name);
+  *out = reinterpret_cast<F>(fn);
+  return LBM_OK;
+}
+
+// Descriptor exchanged between neighbours (lbm_cuboid_p2p_export / _connect).
+struct P2PBlob {
+  char magic[8];
+  int32_t pid, device, rank, world, precision, nx, ny, nzl, ipc_ok, pad;
+  int64_t buf_elems;
+  uint64_t ptr[3];   // buffer 0, buffer 1, flag words (addresses in the exporting process)
+  uint64_t off[3];   // offset of ptr[i] from the base of its allocation
+  cudaIpcMemHandle_t ipc[3];
+};
+static_assert(sizeof(P2PBlob) <= LBM_P2P_BLOB_BYTES, "P2P blob too large");
+constexpr char kBlobMagic[8] = {'L', 'B', 'M', 'P', '2', 'P', '1', 0};
+
+// the halo stream runs after everything already enqueued on the compute stream
+int p2p_fork(lbm_cuboid* h) {
+  CU(cudaEventRecord(h->ev_fork, h->stream));
+  CU(cudaStreamWaitEvent(h->comm_stream, h->ev_fork, 0));
+  return LBM_OK;
+}
+
+// the compute stream continues after the halo stream's work
+int p2p_join(lbm_cuboid* h) {
+  CU(cudaEventRecord(h->ev_bnd, h->comm_stream));
+  CU(cudaStreamWaitEvent(h->stream, h->ev_bnd, 0));
+  return LBM_OK;
+}
+
+// Before publish e + 1 (e = h->epoch): both neighbours have completed publish e,
+// so (i) the ghost planes this slab reads next hold their data of the previous
+// time level and (ii) they no longer read the ghost planes this publish writes
+// (their last reader was their publish e or earlier).  Stream-ordered wait on
+// the flag words in this GPU's memory; nothing spins.
+int p2p_wait(lbm_cuboid* h) {
+  static PfnWaitValue32 wait32 = nullptr;
+  int rc;
+  if (!wait32 && (rc = driver_fn("cuStreamWaitValue32", &wait32))) return rc;
+  const CUstream cs = (CUstream)h->comm_stream;
+  if (h->peer_down >= 0) {
+    CUresult r = wait32(cs, (CUdeviceptr)(h->d_sig + 0), h->epoch, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(LBM_ECUDA, "cuStreamWaitValue32 failed (%d)", int(r));
+  }
+  if (h->peer_up >= 0) {
+    CUresult r = wait32(cs, (CUdeviceptr)(h->d_sig + 1), h->epoch, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) return fail(LBM_ECUDA, "cuStreamWaitValue32 failed (%d)", int(r));
+  }
+  return LBM_OK;
+}
+
+int p2p_ready(const lbm_cuboid* h) {
+  if (!h->p2p_ready) return fail(LBM_EINVAL, "LBM_HALO_P2P: call lbm_cuboid_p2p_connect() on every rank first");
+  return LBM_OK;
+}
+
+// Halo publish of buffer `which` without a collision (init / set_populations).
+int p2p_push(lbm_cuboid* h, int which) {
+  int rc;
+  if ((rc = p2p_ready(h)) || (rc = p2p_fork(h)) || (rc = p2p_wait(h))) return rc;
+  const dim3 g(unsigned((9 * h->nxy + lbm::kBlock - 1) / lbm::kBlock), 2, 1);
+  if (h->p.precision == LBM_FP64)
+    lbm::k_halo_push<double><<<g, lbm::kBlock, 0, h->comm_stream>>>((const double*)h->buf[which], h->c,
+                                                                     p2p_args<double>(h, which, h->epoch + 1));
+  else
+    lbm::k_halo_push<float><<<g, lbm::kBlock, 0, h->comm_stream>>>((const float*)h->buf[which], h->c,
+                                                                    p2p_args<float>(h, which, h->epoch + 1));
+  CU(cudaGetLastError());
+  h->launches++;
+  h->epoch++;
+  return p2p_join(h);
+}
+
+// One time step with the fused halo: boundary planes on the halo stream
+// (storing into the neighbours' ghost planes of buffer cur ^ 1), interior
+// planes concurrently on the compute stream, then join.
+int p2p_step(lbm_cuboid* h) {
+  int rc;
+  if ((rc = p2p_ready(h))) return rc;
+  const int which = h->cur ^ 1;
+  const void* src = h->buf[h->cur];
+  void* dst = h->buf[which];
+  const bool timed = h->timing && h->ev_t.size() < kMaxTimedLaunches;
+  if (timed) {  // one event pair per step around both launches (they overlap)
+    cudaEvent_t a, b;
+    CU(cudaEventCreate(&a));
+    CU(cudaEventCreate(&b));
+    h->ev_t.push_back({a, b});
+    CU(cudaEventRecord(a, h->stream));
+  }
+  if ((rc = p2p_fork(h)) || (rc = p2p_wait(h))) return rc;
+  const int nb = (h->nzl > 1) ? 2 : 1;
+  if ((rc = launch_cs(h, src, dst, 0, nb, std::max(1, h->nzl - 1), h->comm_stream, which, h->epoch + 1, false)))
+    return rc;
+  h->epoch++;
+  if ((rc = launch_cs(h, src, dst, 1, h->nzl - 2, 1, h->stream, -1, 0, false))) return rc;
+  if ((rc = p2p_join(h))) return rc;
+  if (timed) {
+    CU(cudaEventRecord(h->ev_t.back().second, h->stream));
+    h->ev_t_nodes.push_back(int64_t(h->nzl) * h->nxy);
   }
   return LBM_OK;
 }
@@ -510,6 +684,7 @@ int step_once(lbm_cuboid* h) {
   void* src = h->buf[h->cur];
   void* dst = h->buf[h->cur ^ 1];
   if (h->aa) return launch_aa(h, h->stream);
+  if (h->p2p) return p2p_step(h);
   if (!h->ghost) {
     if (h->fd && (rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
     return launch_cs(h, src, dst, 0, h->nzl, 1, h->stream);
@@ -597,6 +772,7 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->paper_rates = (p->omega_1 == 1.0 && p->omega_high == 1.0);
   h->fd = (p->corrections == LBM_CORR_FULL_FD);
   h->aa = (p->streaming == LBM_STREAM_AA);
+  h->p2p = h->ghost && (p->halo == LBM_HALO_P2P);
   fill_consts(h);
 
   auto bail = [&](int code) {
@@ -641,7 +817,23 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
     if (cudaMalloc(&h->d_rho, rb) != cudaSuccess || cudaMemsetAsync(h->d_rho, 0, rb, h->stream) != cudaSuccess)
       return bail(fail(LBM_ENOMEM, "cudaMalloc(%zu) for the density field failed", rb));
   }
-  if (h->ghost) {
+  if (h->p2p) {
+    // the halo stream at the highest priority: its boundary-plane CTAs are
+    // scheduled ahead of the interior CTAs that fill every SM
+    int prio_lo = 0, prio_hi = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+    if (cudaStreamCreateWithPriority(&h->comm_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+      return bail(fail(LBM_ECUDA, "stream/event creation failed"));
+    if (cudaMalloc(&h->d_sig, 4 * sizeof(unsigned int)) != cudaSuccess ||
+        cudaMemsetAsync(h->d_sig, 0, 4 * sizeof(unsigned int), h->stream) != cudaSuccess)
+      return bail(fail(LBM_ENOMEM, "cudaMalloc of the P2P flag words failed"));
+    if (p->world == 1) {  // periodic z on one GPU: this slab is its own neighbour
+      unsigned char blob[LBM_P2P_BLOB_BYTES];
+      if ((rc = lbm_cuboid_p2p_export(h, blob)) || (rc = lbm_cuboid_p2p_connect(h, blob, blob))) return bail(rc);
+    }
+  } else if (h->ghost) {
     if (!p->nccl_uid) return bail(fail(LBM_EINVAL, "nccl_uid is required for the NCCL ghost exchange"));
     // highest priority: the NCCL blocks of the halo are scheduled ahead of the
     // interior collide-stream blocks that otherwise fill every SM's register file
@@ -860,7 +1052,7 @@ int lbm_cuboid_info(const lbm_cuboid_t* h, int64_t out[8]) {
   out[3] = int64_t(2 * 27) * int64_t(h->elem);
   out[4] = h->nxy * h->nzl;
   out[5] = h->buf_elems * int64_t(h->elem);
-  out[6] = h->ghost ? 1 : 0;
+  out[6] = h->ghost ? (h->p2p ? 2 : 1) : 0;
   out[7] = (h->paper_rates && h->p.model == LBM_MODEL_CM) ? 1 : 0;
   return LBM_OK;
 }
@@ -905,11 +1097,133 @@ int lbm_cuboid_timing_read(lbm_cuboid_t* h, double out[3]) {
   return LBM_OK;
 }
 
+int lbm_cuboid_p2p_export(const lbm_cuboid_t* h, void* blob) {
+  if (!h || !blob) return fail(LBM_EINVAL, "NULL argument");
+  if (!h->p2p) return fail(LBM_EINVAL, "the handle does not use the P2P halo (LBM_HALO_P2P with ghost planes)");
+  int rc = set_device(h);
+  if (rc) return rc;
+  PfnAddressRange range = nullptr;
+  if ((rc = driver_fn("cuMemGetAddressRange", &range))) return rc;
+  P2PBlob b;
+  std::memset(&b, 0, sizeof(b));
+  std::memcpy(b.magic, kBlobMagic, sizeof(b.magic));
+  b.pid = int32_t(getpid());
+  b.device = h->p.device;
+  b.rank = h->p.rank;
+  b.world = h->p.world;
+  b.precision = h->p.precision;
+  b.nx = h->p.nx;
+  b.ny = h->p.ny;
+  b.nzl = h->nzl;
+  b.buf_elems = h->buf_elems;
+  b.ipc_ok = 1;
+  void* const ptrs[3] = {h->buf[0], h->buf[1], h->d_sig};
+  for (int i = 0; i < 3; ++i) {
+    b.ptr[i] = (uint64_t)(uintptr_t)ptrs[i];
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)(uintptr_t)ptrs[i]) != CUDA_SUCCESS)
+      return fail(LBM_ECUDA, "cuMemGetAddressRange failed for a P2P buffer");
+    b.off[i] = b.ptr[i] - (uint64_t)base;
+    // IPC handles serve other processes only; a failure (e.g. memory from a
+    // virtual-memory pool) still allows same-process peers
+    if (cudaIpcGetMemHandle(&b.ipc[i], (void*)(uintptr_t)base) != cudaSuccess) {
+      cudaGetLastError();
+      b.ipc_ok = 0;
+    }
+  }
+  std::memset(blob, 0, LBM_P2P_BLOB_BYTES);
+  std::memcpy(blob, &b, sizeof(b));
+  return LBM_OK;
+}
+
+int lbm_cuboid_p2p_connect(lbm_cuboid_t* h, const void* blob_down, const void* blob_up) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  if (!h->p2p) return fail(LBM_EINVAL, "the handle does not use the P2P halo (LBM_HALO_P2P with ghost planes)");
+  if (h->p2p_ready) return fail(LBM_EINVAL, "lbm_cuboid_p2p_connect: already connected");
+  int rc = set_device(h);
+  if (rc) return rc;
+  const void* blobs[2] = {blob_down, blob_up};
+  const int peers[2] = {h->peer_down, h->peer_up};
+  P2PBlob b[2];
+  for (int side = 0; side < 2; ++side) {
+    if (peers[side] < 0) continue;  // no neighbour on this side: blob ignored
+    if (!blobs[side]) return fail(LBM_EINVAL, "the %s neighbour (rank %d) needs a blob", side ? "up" : "down",
+                                  peers[side]);
+    std::memcpy(&b[side], blobs[side], sizeof(P2PBlob));
+    const P2PBlob& x = b[side];
+    if (std::memcmp(x.magic, kBlobMagic, sizeof(kBlobMagic)) != 0)
+      return fail(LBM_EINVAL, "not a lbm_cuboid P2P blob");
+    if (x.rank != peers[side] || x.world != h->p.world)
+      return fail(LBM_EINVAL, "blob of rank %d/%d given for the %s neighbour, expected rank %d/%d", x.rank, x.world,
+                  side ? "up" : "down", peers[side], h->p.world);
+    if (x.nx != h->p.nx || x.ny != h->p.ny || x.nzl != h->nzl || x.precision != h->p.precision ||
+        x.buf_elems != h->buf_elems)
+      return fail(LBM_EINVAL, "neighbour blob has another geometry or precision");
+  }
+  // map (a rank that is both neighbours is mapped once)
+  void* m[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  const pid_t me = getpid();
+  for (int side = 0; side < 2; ++side) {
+    if (peers[side] < 0) continue;
+    const P2PBlob& x = b[side];
+    if (side == 1 && peers[0] >= 0 && b[0].pid == x.pid && b[0].ptr[0] == x.ptr[0] && b[0].ptr[2] == x.ptr[2]) {
+      for (int i = 0; i < 3; ++i) m[1][i] = m[0][i];
+      continue;
+    }
+    if (x.pid == int32_t(me)) {  // same process: direct pointers (peer access if another device)
+      if (x.device != h->p.device) {
+        int ok = 0;
+        CU(cudaDeviceCanAccessPeer(&ok, h->p.device, x.device));
+        if (!ok) return fail(LBM_ECUDA, "device %d cannot access peer device %d", h->p.device, x.device);
+        cudaError_t e = cudaDeviceEnablePeerAccess(x.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CU(e);
+        cudaGetLastError();
+      }
+      for (int i = 0; i < 3; ++i) m[side][i] = (void*)(uintptr_t)x.ptr[i];
+    } else {
+      if (!x.ipc_ok) return fail(LBM_EINVAL, "the neighbour's buffers cannot be shared between processes (no IPC)");
+      for (int i = 0; i < 3; ++i) {
+        void* base = nullptr;
+        CU(cudaIpcOpenMemHandle(&base, x.ipc[i], cudaIpcMemLazyEnablePeerAccess));
+        h->ipc_open.push_back(base);
+        m[side][i] = (char*)base + x.off[i];
+      }
+    }
+  }
+  for (int i = 0; i < 2; ++i) {
+    h->peer_buf_dn[i] = m[0][i];
+    h->peer_buf_up[i] = m[1][i];
+  }
+  // flag words: [0] is written by the slab below, [1] by the slab above
+  h->peer_flag_dn = peers[0] >= 0 ? (unsigned int*)m[0][2] + 1 : nullptr;
+  h->peer_flag_up = peers[1] >= 0 ? (unsigned int*)m[1][2] + 0 : nullptr;
+  h->p2p_ready = true;
+  return LBM_OK;
+}
+
 int lbm_cuboid_destroy(lbm_cuboid_t* h) {
   if (!h) return LBM_OK;
   cudaSetDevice(h->p.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   if (h->comm_stream) cudaStreamSynchronize(h->comm_stream);
+  if (h->p2p_ready) {
+    // no neighbour store into this slab may be in flight when it is freed: wait
+    // (host side, bounded) until both neighbours have published this epoch
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      unsigned int sig[2] = {0, 0};
+      if (cudaMemcpy(sig, h->d_sig, sizeof(sig), cudaMemcpyDeviceToHost) != cudaSuccess) break;
+      const bool dn = h->peer_down < 0 || int32_t(sig[0] - h->epoch) >= 0;
+      const bool up = h->peer_up < 0 || int32_t(sig[1] - h->epoch) >= 0;
+      if (dn && up) break;
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(30)) break;
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    }
+    for (void* m : h->ipc_open) cudaIpcCloseMemHandle(m);
+  }
+  if (h->d_sig) cudaFree(h->d_sig);
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->comm) ncclCommDestroy(h->comm);
   if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
   if (h->ev_halo) cudaEventDestroy(h->ev_halo);

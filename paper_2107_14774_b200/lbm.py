@@ -22,13 +22,14 @@ LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EUNSTABLE, LBM_ENOTSUP
 BC_PERIODIC, BC_BOUNCE_BACK, BC_MOVING_WALL, BC_FREE_SLIP = 0, 1, 2, 3
 CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF, CORR_FULL_FD = 0, 1, 2, 3
 FP64, FP32_STORAGE = 0, 1
-HALO_AUTO, HALO_NCCL = 0, 1
+HALO_AUTO, HALO_NCCL, HALO_P2P = 0, 1, 2
+P2P_BLOB_BYTES = 512
 MODEL_CM, MODEL_RM = 0, 1
 STREAM_AB, STREAM_AA = 0, 1
 
 # every symbol include/lbm_cuboid.h declares
 EXPORTS = ["lbm_cuboid_default_params", "lbm_cuboid_buffer_bytes", "lbm_cuboid_halo_plan",
-           "lbm_cuboid_nccl_unique_id",
+           "lbm_cuboid_nccl_unique_id", "lbm_cuboid_p2p_export", "lbm_cuboid_p2p_connect",
            "lbm_cuboid_create", "lbm_cuboid_init_fields", "lbm_cuboid_init_fields_device",
            "lbm_cuboid_step", "lbm_cuboid_sync", "lbm_cuboid_get_macroscopic",
            "lbm_cuboid_get_macroscopic_device", "lbm_cuboid_get_populations",
@@ -77,6 +78,8 @@ def load():
     L.lbm_cuboid_halo_plan.argtypes = [ctypes.POINTER(Params), ctypes.POINTER(ctypes.c_int64)]
     L.lbm_cuboid_nccl_unique_id.argtypes = [ctypes.c_char_p]
     L.lbm_cuboid_create.argtypes = [ctypes.POINTER(Params), ctypes.POINTER(_VP)]
+    L.lbm_cuboid_p2p_export.argtypes = [_VP, ctypes.c_char_p]
+    L.lbm_cuboid_p2p_connect.argtypes = [_VP, ctypes.c_char_p, ctypes.c_char_p]
     for n in ("lbm_cuboid_init_fields", "lbm_cuboid_init_fields_device", "lbm_cuboid_get_macroscopic",
               "lbm_cuboid_get_macroscopic_device"):
         getattr(L, n).argtypes = [_VP, _VP, _VP]
@@ -98,6 +101,7 @@ def load():
     for name in EXPORTS:
         getattr(L, name)
     for n in ("lbm_cuboid_buffer_bytes", "lbm_cuboid_halo_plan", "lbm_cuboid_nccl_unique_id", "lbm_cuboid_create",
+              "lbm_cuboid_p2p_export", "lbm_cuboid_p2p_connect",
               "lbm_cuboid_init_fields", "lbm_cuboid_init_fields_device", "lbm_cuboid_step",
               "lbm_cuboid_sync", "lbm_cuboid_get_macroscopic", "lbm_cuboid_get_macroscopic_device",
               "lbm_cuboid_get_populations", "lbm_cuboid_get_populations_planes",
@@ -286,8 +290,18 @@ class Lattice:
         a = (ctypes.c_int64 * 8)()
         _check(load().lbm_cuboid_info(self._h, a))
         keys = ["launches", "collide_stream_launches", "steps", "bytes_per_node_update",
-                "local_nodes", "buffer_bytes", "nccl_halo", "paper_rate_kernel"]
+                "local_nodes", "buffer_bytes", "halo", "paper_rate_kernel"]
         return dict(zip(keys, list(a)))
+
+    def p2p_export(self) -> bytes:
+        """This slab's LBM_HALO_P2P descriptor (IPC handles + addresses), for its neighbours."""
+        buf = ctypes.create_string_buffer(P2P_BLOB_BYTES)
+        _check(load().lbm_cuboid_p2p_export(self._h, buf))
+        return buf.raw
+
+    def p2p_connect(self, blob_down: bytes | None, blob_up: bytes | None):
+        """Map the neighbours' buffers (None where halo_plan has no neighbour)."""
+        _check(load().lbm_cuboid_p2p_connect(self._h, blob_down, blob_up))
 
     def timing(self, enable: bool):
         """Enable/disable (and clear) per-launch CUDA-event timing of the collide-stream kernel."""
@@ -310,12 +324,28 @@ class Lattice:
             pass
 
 
+def p2p_neighbour_blobs(plan: dict, blobs: list) -> tuple:
+    """(blob_down, blob_up) for lbm_cuboid_p2p_connect from every rank's blob
+    (index = rank) and this rank's halo plan."""
+    dn, up = int(plan["peer_down"]), int(plan["peer_up"])
+    return (blobs[dn] if dn >= 0 else None, blobs[up] if up >= 0 else None)
+
+
 def distributed_lattice(**kw) -> Lattice:
     """Create this rank's slab under an initialised torch.distributed process
-    group: rank 0 makes the NCCL unique id, the group broadcasts it."""
+    group.  NCCL halo: rank 0 makes the NCCL unique id, the group broadcasts
+    it.  P2P halo (halo=HALO_P2P): every rank exports its descriptor, the group
+    all-gathers them and each rank maps its two neighbours."""
     import torch.distributed as dist  # noqa: PLC0415
 
     world, rank = dist.get_world_size(), dist.get_rank()
+    if int(kw.get("halo", HALO_AUTO)) == HALO_P2P:
+        lat = Lattice(rank=rank, world=world, **kw)
+        if world > 1:
+            blobs = [None] * world
+            dist.all_gather_object(blobs, lat.p2p_export())
+            lat.p2p_connect(*p2p_neighbour_blobs(halo_plan(lat.p), blobs))
+        return lat
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     return Lattice(rank=rank, world=world, nccl_uid=obj[0], **kw)

@@ -159,7 +159,7 @@ def test_nccl_self_halo_matches_wrap(P):
     a = _gpu(P, w)
     uid = P.nccl_unique_id()
     b = _gpu(P, w, halo=P.HALO_NCCL, nccl_uid=uid)
-    assert b.info()["nccl_halo"] == 1 and a.info()["nccl_halo"] == 0
+    assert b.info()["halo"] == 1 and a.info()["halo"] == 0
     a.init_fields(rho, u)
     b.init_fields(rho, u)
     a.step(40)
