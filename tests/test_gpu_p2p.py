@@ -218,3 +218,26 @@ def test_p2p_wiring_errors(P):
     nohalo.close()
     # hs[0] is connected but hs[1] is not: close without publishing (epoch 0)
     _close(hs)
+
+
+@pytest.mark.parametrize("world,case", [(2, "periodic"), (3, "walls"), (4, "periodic")])
+def test_p2p_cuda_ipc_between_processes(P, world, case):
+    """The CUDA-IPC wiring (cudaIpcGetMemHandle / cudaIpcOpenMemHandle of the
+    torch-allocated buffers and the flag words) between `world` processes on one
+    GPU, stepped one rank at a time (scripts/p2p_ipc_check.py)."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(root, "scripts", "p2p_ipc_check.py"), "--case", case]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert '"bitwise_equal": true' in r.stdout, r.stdout

@@ -82,3 +82,52 @@ def test_gloo_halo_exchange_matches_global_pull(world, bcz):
     mp.start_processes(_worker, args=(world, _free_port(), bcz, res), nprocs=world, join=True,
                        start_method="spawn")
     assert dict(res) == {r: True for r in range(world)}
+
+
+def _p2p_worker(rank, world, port, bcz, result):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2107_14774_b200 as P
+
+    p = P.lbm.make_params(4, 3, 2 * world, 1.0, 2.0, omega_nu=1.5, world=world, rank=rank,
+                          bc=(0, 0, 0, 0, bcz, bcz), halo=P.HALO_P2P)
+    hp = P.lbm.halo_plan(p)
+    blobs = [None] * world
+    dist.all_gather_object(blobs, f"blob-of-rank-{rank}".encode())
+    dn, up = P.lbm.p2p_neighbour_blobs(hp, blobs)
+    plans = [None] * world
+    dist.all_gather_object(plans, hp)
+    ok = bool(hp["ghost"])
+    # the blob picked for each side is the neighbour's own
+    ok &= (dn is None) == (hp["peer_down"] < 0) and (up is None) == (hp["peer_up"] < 0)
+    if dn is not None:
+        ok &= dn == f"blob-of-rank-{hp['peer_down']}".encode()
+    if up is not None:
+        ok &= up == f"blob-of-rank-{hp['peer_up']}".encode()
+    # symmetry: my up neighbour's down neighbour is me (its flag word [0] is mine)
+    if hp["peer_up"] >= 0:
+        ok &= plans[hp["peer_up"]]["peer_down"] == rank
+    if hp["peer_down"] >= 0:
+        ok &= plans[hp["peer_down"]]["peer_up"] == rank
+    # the region a rank stores into its up neighbour (send_up) lands at the
+    # neighbour's recv_down offset, plane nz_l above: same q block, ghost p = 0
+    nxy, nzl = 12, 2
+    ok &= hp["send_up"] - nzl * 27 * nxy == hp["recv_down"]
+    ok &= hp["send_down"] + nzl * 27 * nxy == hp["recv_up"]
+    result[rank] = ok
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,bcz", [(2, 0), (3, 1), (4, 0)])
+def test_gloo_p2p_neighbour_wiring(world, bcz):
+    """Host logic of the fused P2P halo under a real process group: descriptor
+    all-gather, neighbour selection from the halo plan, symmetric flag slots and
+    the store offsets the boundary kernel uses."""
+    from paper_2107_14774_b200 import build as B
+
+    B.build()
+    mgr = mp.Manager()
+    res = mgr.dict()
+    mp.start_processes(_p2p_worker, args=(world, _free_port(), bcz, res), nprocs=world, join=True,
+                       start_method="spawn")
+    assert dict(res) == {r: True for r in range(world)}
