@@ -121,9 +121,11 @@ typedef struct {
                                   [rank*nz/world, (rank+1)*nz/world) */
   int32_t device;              /* CUDA device ordinal of this rank */
   int32_t halo;                /* lbm_halo */
-  int32_t graphs;              /* CUDA graphs for step(n): 0 auto (replay captured 32-step graphs when
-                                  the slab has < 4M nodes and no ghost exchange), 1 never, 2 always
-                                  (when no ghost exchange) */
+  int32_t graphs;              /* launch mode of step(n): 0 auto (replay captured 32-step CUDA graphs when
+                                  the slab has < 4M nodes and no ghost exchange), 1 one stream launch per
+                                  step, 2 always graphs (when no ghost exchange), 3 persistent cooperative
+                                  kernel running up to 1024 steps per launch with a grid-wide barrier
+                                  between steps (single GPU, no ghost exchange, not AA) */
   int32_t model;               /* lbm_model */
   int32_t streaming;           /* lbm_streaming; with LBM_STREAM_AA only buf_a is used */
   const void *nccl_uid;        /* 128-byte ncclUniqueId from lbm_cuboid_nccl_unique_id() on rank 0,

@@ -15,6 +15,7 @@
 // transforms is three passes of nine 3-point transforms, all in registers.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -958,6 +959,56 @@ __global__ void __launch_bounds__(kBlock) k_halo_push(const T* __restrict__ src,
       a.up[18LL * c.nxy + e] = src[(long long)c.nzl * c.plane + 18LL * c.nxy + e];
   }
   p2p_signal(a);
+}
+
+// ------------------------------------ persistent multi-step kernel (small lattices)
+// The paper's own grids are small (27k-2M nodes): both population
+// buffers then sit in the 126 MB L2 and a step is a few microseconds, so the
+// per-launch cost dominates.  One cooperative launch of co-resident CTAs runs
+// nsteps time steps; each CTA walks the nodes grid-stride (x fastest: coalesced)
+// and a grid-wide barrier separates the steps (and, for FULL_FD, the density
+// pass from the collision).  Per node the arithmetic is collide_stream_ab's
+// (same gather, core and store), so results are bitwise those of one launch per
+// step.  Single GPU, no ghost exchange.
+template <typename T, int KIND, bool FD>
+__global__ void LBM_CS_BOUNDS k_persistent(T* __restrict__ b0, T* __restrict__ b1, double* __restrict__ rf,
+                                           const __grid_constant__ Consts c, int cur, int nsteps) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const long long nodes = (long long)c.nzl * c.nxy;
+  const long long stride = (long long)gridDim.x * kBlock;
+  const long long first = (long long)blockIdx.x * kBlock + threadIdx.x;
+  for (int t = 0; t < nsteps; ++t) {
+    const bool odd = ((cur + t) & 1) != 0;
+    const T* src = odd ? b1 : b0;
+    T* dst = odd ? b0 : b1;
+    if (FD) {
+      for (long long n = first; n < nodes; n += stride) {
+        const int z = int(n / c.nxy);
+        const int idx = int(n - (long long)z * c.nxy);
+        const int y = idx / c.nx;
+        double f[27];
+        gather<T>(src, c, idx - y * c.nx, y, z, f);
+        double r0 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 27; ++q) r0 += f[q];
+        rf[(long long)(z + 1) * c.nxy + idx] = r0;
+      }
+      grid.sync();
+    }
+    for (long long n = first; n < nodes; n += stride) {
+      const int z = int(n / c.nxy);
+      const int idx = int(n - (long long)z * c.nxy);
+      const int y = idx / c.nx;
+      const int x = idx - y * c.nx;
+      double gxr = 0.0, gyr = 0.0, gzr = 0.0;
+      if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
+      double f[27];
+      gather<T>(src, c, x, y, z, f);
+      StoreOwn<T> st{dst, dst + (long long)(z + 1) * c.plane + idx, c.nxy, &c};
+      run_core<KIND, FD>(c, f, gxr, gyr, gzr, st);
+    }
+    if (t + 1 < nsteps) grid.sync();
+  }
 }
 
 // ------------------------------------------------ AA in-place streaming (one buffer)

@@ -67,6 +67,8 @@ constexpr size_t kStageBytes = size_t(256) << 20;  // host<->device staging chun
 constexpr size_t kMaxTimedLaunches = 1 << 16;
 constexpr int kGraphSteps = 32;                 // steps per captured graph (even: ends on the same buffer)
 constexpr int64_t kGraphMaxNodes = 4 << 20;     // auto mode: graphs below this many local nodes
+constexpr int64_t kPersistMaxNodes = 0;          // auto mode: persistent kernel up to this many nodes
+constexpr int kPersistChunk = 1024;              // steps per persistent launch
 
 }  // namespace
 
@@ -149,7 +151,7 @@ int validate(const lbm_cuboid_params* p) {
   if (p->halo < 0 || p->halo > 2) return fail(LBM_EINVAL, "halo must be an lbm_halo");
   if (p->halo == LBM_HALO_P2P && p->corrections == LBM_CORR_FULL_FD)
     return fail(LBM_ENOTSUP, "LBM_HALO_P2P does not support FULL_FD (use LBM_HALO_NCCL)");
-  if (p->graphs < 0 || p->graphs > 2) return fail(LBM_EINVAL, "graphs must be 0, 1 or 2");
+  if (p->graphs < 0 || p->graphs > 3) return fail(LBM_EINVAL, "graphs must be 0, 1, 2 or 3");
   if (p->model < 0 || p->model > 1) return fail(LBM_EINVAL, "model must be an lbm_model");
   if (p->streaming < 0 || p->streaming > 1) return fail(LBM_EINVAL, "streaming must be an lbm_streaming");
   if (p->streaming == LBM_STREAM_AA) {
@@ -398,9 +400,64 @@ void drop_graphs(lbm_cuboid* h) {
     }
 }
 
+bool use_persistent(const lbm_cuboid* h) {
+  if (h->ghost || h->aa) return false;
+  return h->p.graphs == 3 || (h->p.graphs == 0 && h->nxy * h->nzl <= kPersistMaxNodes);
+}
+
 bool use_graphs(const lbm_cuboid* h) {
-  if (h->ghost || h->timing || h->p.graphs == 1) return false;
+  if (h->ghost || h->timing || h->p.graphs == 1 || h->p.graphs == 3) return false;
   return h->p.graphs == 2 || h->nxy * h->nzl < kGraphMaxNodes;
+}
+
+template <typename T>
+const void* persistent_fn(int kind, bool fd) {
+  using namespace lbm;
+  if (kind == CORE_PAPER) return fd ? (const void*)k_persistent<T, CORE_PAPER, true> : (const void*)k_persistent<T, CORE_PAPER, false>;
+  if (kind == CORE_RAW) return fd ? (const void*)k_persistent<T, CORE_RAW, true> : (const void*)k_persistent<T, CORE_RAW, false>;
+  return fd ? (const void*)k_persistent<T, CORE_GENERIC, true> : (const void*)k_persistent<T, CORE_GENERIC, false>;
+}
+
+// nsteps steps in cooperative launches of at most kPersistChunk steps, each with
+// as many CTAs as can be co-resident (capped at one node per thread)
+int launch_persistent(lbm_cuboid* h, int64_t nsteps) {
+  const int kind = (h->p.model == LBM_MODEL_RM) ? lbm::CORE_RAW : (h->paper_rates ? lbm::CORE_PAPER : lbm::CORE_GENERIC);
+  const bool fp64 = (h->p.precision == LBM_FP64);
+  const void* fn = fp64 ? persistent_fn<double>(kind, h->fd) : persistent_fn<float>(kind, h->fd);
+  int per_sm = 0, sms = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, lbm::kBlock, 0));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->p.device));
+  const int64_t nodes = h->nxy * h->nzl;
+  const int64_t want = (nodes + lbm::kBlock - 1) / lbm::kBlock;
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(want, int64_t(per_sm) * sms)));
+  if (per_sm < 1) return fail(LBM_ECUDA, "persistent kernel cannot be resident");
+  while (nsteps > 0) {
+    int n = int(std::min<int64_t>(nsteps, kPersistChunk));
+    int cur = h->cur;
+    void* b0 = h->buf[0];
+    void* b1 = h->buf[1];
+    double* rf = h->d_rho;
+    void* args[] = {&b0, &b1, &rf, (void*)&h->c, &cur, &n};
+    const bool timed = h->timing && h->ev_t.size() < kMaxTimedLaunches;
+    if (timed) {
+      cudaEvent_t a, b;
+      CU(cudaEventCreate(&a));
+      CU(cudaEventCreate(&b));
+      h->ev_t.push_back({a, b});
+      CU(cudaEventRecord(a, h->stream));
+    }
+    CU(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(lbm::kBlock), args, 0, h->stream));
+    if (timed) {
+      CU(cudaEventRecord(h->ev_t.back().second, h->stream));
+      h->ev_t_nodes.push_back(int64_t(n) * nodes);
+    }
+    h->launches++;
+    h->cs_launches++;
+    h->steps += n;
+    if (n & 1) h->cur ^= 1;
+    nsteps -= n;
+  }
+  return LBM_OK;
 }
 
 int step_once(lbm_cuboid* h);
@@ -894,6 +951,7 @@ int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
   if (nsteps < 0) return fail(LBM_EINVAL, "nsteps must be >= 0");
   int rc = set_device(h);
   if (rc) return rc;
+  if (use_persistent(h)) return launch_persistent(h, nsteps);
   if (use_graphs(h)) {
     while (nsteps >= kGraphSteps) {
       if (!h->gexec[h->cur] && (rc = capture_graph(h, h->cur))) return rc;

@@ -530,3 +530,45 @@ def test_aa_rejects_multi_gpu_and_fd(P):
         _gpu(P, w, streaming=P.STREAM_AA, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id())
     with pytest.raises(P.LbmError):
         _gpu(P, w.scaled(corrections=synth.CORR_FULL_FD), streaming=P.STREAM_AA)
+
+
+PERSIST_CASES = {
+    "tgv_paper": (synth.CONFIGS["tgv"], {}),
+    "cavity_generic": (synth.CONFIGS["cavity100"].scaled(nx=21, ny=19, nz=11), {"omega_1": 1.2, "omega_high": 1.1}),
+    "shear_raw_fp32": (synth.CONFIGS["shear"].scaled(nx=16, ny=29, nz=12), {"model": 1, "precision": 1}),
+    "duct_fd": (synth.CONFIGS["duct"].scaled(nx=5, ny=37, nz=19), {"corrections": 3}),
+    "tgv_fd_fp32": (synth.CONFIGS["tgv"].scaled(nx=24, ny=20, nz=10), {"corrections": 3, "precision": 1}),
+}
+
+
+@pytest.mark.parametrize("case", list(PERSIST_CASES))
+def test_persistent_kernel_bitwise_equal_to_launches(P, case):
+    """graphs = 3 (one cooperative launch for many steps, grid barrier between
+    steps) gives bitwise the per-step launches' result; odd step counts."""
+    w, kw = PERSIST_CASES[case]
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 41)
+    a = _gpu(P, w, graphs=1, **kw)
+    b = _gpu(P, w, graphs=3, **kw)
+    for g in (a, b):
+        g.init_fields(rho, u)
+        g.step(37)
+        g.step(0)
+        g.step(2)
+    assert np.array_equal(a.get_populations(), b.get_populations())
+    assert b.info()["steps"] == 39 and b.info()["collide_stream_launches"] == 2
+    a.close()
+    b.close()
+
+
+def test_persistent_kernel_long_run_chunks_and_oracle(P):
+    """More steps than one persistent launch holds (1024): chunked launches,
+    buffer parity across chunks, against the oracle on config 1."""
+    w = synth.CONFIGS["tgv"].scaled(nx=12, ny=10, nz=6)
+    o, g = _init_both(P, w, seed=8, noneq=1e-3, graphs=3)
+    g.timing(True)
+    g.step(1031)
+    t = g.timing_read()
+    assert t["launches"] == 2 and t["node_updates"] == 1031 * w.nodes
+    o.step(1031)
+    _cmp(o, g)
+    g.close()
