@@ -366,20 +366,16 @@ __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int
 // difference 1/(2c) weighted by the rest weights of the two other axes.  A
 // neighbour across a wall face takes the node's own density.  rf has the
 // population-buffer plane structure: rf[(z_local + 1) * nxy + y * nx + x].
-__device__ __forceinline__ void density_gradient(const double* __restrict__ rf, const Consts& c, int x, int y,
-                                                 int z, double& gx, double& gy, double& gz) {
-  const int nx = c.nx;
+// rho_at(i, j, k) = density at offset (i-1, j-1, k-1) from the node (never
+// called for a neighbour across a wall); identical arithmetic for every source.
+template <class RhoAt>
+__device__ __forceinline__ void density_gradient_g(const Consts& c, int x, int y, int z, RhoAt rho_at, double& gx,
+                                                   double& gy, double& gz) {
   auto is_wall = [](int fk) { return fk >= FK_BOUNCE && fk <= FK_SLIP; };
-  const int xs[3] = {(x == 0) ? nx - 1 : x - 1, x, (x == nx - 1) ? 0 : x + 1};
-  const bool cx[3] = {x == 0 && is_wall(c.face[0]), false, x == nx - 1 && is_wall(c.face[1])};
-  const int ys[3] = {((y == 0) ? c.ny - 1 : y - 1) * nx, y * nx, ((y == c.ny - 1) ? 0 : y + 1) * nx};
+  const bool cx[3] = {x == 0 && is_wall(c.face[0]), false, x == c.nx - 1 && is_wall(c.face[1])};
   const bool cy[3] = {y == 0 && is_wall(c.face[2]), false, y == c.ny - 1 && is_wall(c.face[3])};
-  int zm = z - 1, zp = z + 1;
-  if (z == 0 && c.face[4] == FK_WRAP) zm = c.nzl - 1;
-  if (z == c.nzl - 1 && c.face[5] == FK_WRAP) zp = 0;
-  const long long zb[3] = {(long long)(zm + 1) * c.nxy, (long long)(z + 1) * c.nxy, (long long)(zp + 1) * c.nxy};
   const bool cz[3] = {z == 0 && is_wall(c.face[4]), false, z == c.nzl - 1 && is_wall(c.face[5])};
-  const double own = __ldg(rf + zb[1] + ys[1] + xs[1]);
+  const double own = rho_at(1, 1, 1);
   double sx = 0.0, sy = 0.0, sz = 0.0;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
@@ -389,7 +385,7 @@ __device__ __forceinline__ void density_gradient(const double* __restrict__ rf, 
       for (int i = 0; i < 3; ++i) {
         if (i == 1 && j == 1 && k == 1) continue;
         const bool wall = cx[i] || cy[j] || cz[k];
-        const double v = wall ? own : __ldg(rf + zb[k] + ys[j] + xs[i]);
+        const double v = wall ? own : rho_at(i, j, k);
         if (i != 1) sx += (i == 2 ? 1.0 : -1.0) * c.phy[j] * c.phz[k] * v;
         if (j != 1) sy += (j == 2 ? 1.0 : -1.0) * c.phx[i] * c.phz[k] * v;
         if (k != 1) sz += (k == 2 ? 1.0 : -1.0) * c.phx[i] * c.phy[j] * v;
@@ -397,6 +393,19 @@ __device__ __forceinline__ void density_gradient(const double* __restrict__ rf, 
   gx = 0.5 * sx;
   gy = c.h1y * sy;
   gz = c.h1z * sz;
+}
+
+__device__ __forceinline__ void density_gradient(const double* __restrict__ rf, const Consts& c, int x, int y,
+                                                 int z, double& gx, double& gy, double& gz) {
+  const int nx = c.nx;
+  const int xs[3] = {(x == 0) ? nx - 1 : x - 1, x, (x == nx - 1) ? 0 : x + 1};
+  const int ys[3] = {((y == 0) ? c.ny - 1 : y - 1) * nx, y * nx, ((y == c.ny - 1) ? 0 : y + 1) * nx};
+  int zm = z - 1, zp = z + 1;
+  if (z == 0 && c.face[4] == FK_WRAP) zm = c.nzl - 1;
+  if (z == c.nzl - 1 && c.face[5] == FK_WRAP) zp = 0;
+  const long long zb[3] = {(long long)(zm + 1) * c.nxy, (long long)(z + 1) * c.nxy, (long long)(zp + 1) * c.nxy};
+  density_gradient_g(
+      c, x, y, z, [&](int i, int j, int k) { return __ldg(rf + zb[k] + ys[j] + xs[i]); }, gx, gy, gz);
 }
 
 // density pass for FULL_FD: rho(x, t+1) = sum_q f_q(x, t+1) of the pulled populations
@@ -414,6 +423,61 @@ __global__ void __launch_bounds__(kBlock) k_density(const T* __restrict__ src, d
 #pragma unroll
   for (int q = 0; q < 27; ++q) r0 += f[q];
   rho_out[(long long)(z + 1) * c.nxy + idx] = r0;
+}
+
+// ------------------------------------- fused FULL_FD collide-stream (2.5D blocking)
+// FULL_FD needs the same-time density of the 26 neighbours, i.e. their pulled
+// populations.  Instead of a separate density pass (+216 B/node of HBM reads
+// and a density field), a CTA owns a kFdTx x kFdTy tile of one z-chunk and
+// marches up the chunk: at plane p it gathers the pulled populations of the
+// tile and its one-node ring (periodic wrap; ghost planes from the exchanged
+// density field), sums them to rho and keeps rho of the last four planes in a
+// shared-memory ring; then it collides plane p - 1 with the gradient read from
+// shared memory, re-gathering the node's own populations (an L2 hit: the same
+// CTA read them one plane earlier).  Every population comes from HBM once
+// (plus the 2/kFdZc chunk overlap), the neighbour reuse of rho lives in shared
+// memory, and the arithmetic is density_gradient's and k_density's, so the
+// result is bitwise that of the two-pass path.
+#ifndef LBM_FD_ZC
+#define LBM_FD_ZC 32  // planes per z-chunk
+#endif
+#ifndef LBM_FD_TY
+#define LBM_FD_TY 4   // tile rows (tile = 32 x LBM_FD_TY nodes, one thread each)
+#endif
+#ifndef LBM_FD_MINB
+#define LBM_FD_MINB 4 // resident CTAs per SM requested from ptxas
+#endif
+#ifndef LBM_FD_TX
+#define LBM_FD_TX 32  // tile columns
+#endif
+constexpr int kFdTx = LBM_FD_TX, kFdTy = LBM_FD_TY, kFdThreads = kFdTx * kFdTy, kFdZc = LBM_FD_ZC;
+constexpr int kFdRw = kFdTx + 2, kFdRing = (kFdTx + 2) * (kFdTy + 2);
+
+// rho(t+1) at node (gx, gy, p) of the tile ring (coordinates may lie one node
+// outside the slab/grid); 0 where no active node of the tile needs it (across
+// a wall, or beyond a partial tile)
+template <typename T>
+__device__ __forceinline__ double ring_rho(const T* src, const double* rf, const Consts& c, int gx, int gy, int p) {
+  if (gx < 0 || gx >= c.nx) {
+    if (c.face[0] != FK_WRAP || gx < -1 || gx > c.nx) return 0.0;
+    gx = (gx < 0) ? c.nx - 1 : 0;
+  }
+  if (gy < 0 || gy >= c.ny) {
+    if (c.face[2] != FK_WRAP || gy < -1 || gy > c.ny) return 0.0;
+    gy = (gy < 0) ? c.ny - 1 : 0;
+  }
+  if (p < 0 || p >= c.nzl) {
+    const int fk = c.face[p < 0 ? 4 : 5];
+    if (fk == FK_GHOST) return __ldg(rf + (long long)(p + 1) * c.nxy + gy * c.nx + gx);
+    if (fk != FK_WRAP) return 0.0;
+    p = (p < 0) ? c.nzl - 1 : 0;
+  }
+  double f[27];
+  gather<T>(src, c, gx, gy, p, f);
+  double r0 = 0.0;
+#pragma unroll
+  for (int q = 0; q < 27; ++q) r0 += f[q];
+  return r0;
 }
 
 // --------------------------------------------------------- store policies
@@ -857,6 +921,48 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T*
                                                    const double* __restrict__ rf, const __grid_constant__ Consts c,
                                                    int zbeg, int zstride) {
   collide_stream_ab<T, CORE_RAW, FD>(src, dst, rf, c, zbeg, zstride);
+}
+
+// chunk blockIdx.z covers planes [z0, z1), z0 = zbeg + blockIdx.z * zstride,
+// z1 = min(z0 + zlen, zend)
+template <typename T, int KIND>
+__device__ __forceinline__ void collide_stream_fd_fused(const T* __restrict__ src, T* __restrict__ dst,
+                                                        const double* __restrict__ rf, const Consts& c, int zbeg,
+                                                        int zstride, int zlen, int zend) {
+  __shared__ double srho[4][kFdTy + 2][kFdRw];
+  const int tx = threadIdx.x % kFdTx, ty = threadIdx.x / kFdTx;
+  const int x0 = blockIdx.x * kFdTx, y0 = blockIdx.y * kFdTy;
+  const int z0 = zbeg + blockIdx.z * zstride;
+  const int z1 = min(z0 + zlen, zend);
+  const int x = x0 + tx, y = y0 + ty;
+  const bool active = (x < c.nx) && (y < c.ny);
+  for (int p = z0 - 1; p <= z1; ++p) {
+    // four slots: the slot written here was last read two planes ago, and this
+    // iteration's barrier separates the two (one barrier per plane)
+    for (int pos = threadIdx.x; pos < kFdRing; pos += kFdThreads) {
+      const int ly = pos / kFdRw, lx = pos - ly * kFdRw;
+      srho[p & 3][ly][lx] = ring_rho<T>(src, rf, c, x0 + lx - 1, y0 + ly - 1, p);
+    }
+    __syncthreads();
+    if (p > z0 && active) {
+      const int z = p - 1;
+      double gxr, gyr, gzr;
+      density_gradient_g(
+          c, x, y, z, [&](int i, int j, int k) { return srho[(z + k - 1) & 3][ty + j][tx + i]; }, gxr, gyr, gzr);
+      double f[27];
+      gather<T>(src, c, x, y, z, f);
+      const int idx = y * c.nx + x;
+      StoreOwn<T> st{dst, dst + (long long)(z + 1) * c.plane + idx, c.nxy, &c};
+      run_core<KIND, true>(c, f, gxr, gyr, gzr, st);
+    }
+  }
+}
+
+template <typename T, int KIND>
+__global__ void __launch_bounds__(kFdThreads, LBM_FD_MINB)
+    k_collide_stream_fd(const T* __restrict__ src, T* __restrict__ dst, const double* __restrict__ rf,
+                        const __grid_constant__ Consts c, int zbeg, int zstride, int zlen, int zend) {
+  collide_stream_fd_fused<T, KIND>(src, dst, rf, c, zbeg, zstride, zlen, zend);
 }
 
 // ------------------------------------ fused collide-stream + peer-memory halo (P2P)

@@ -28,6 +28,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -87,6 +88,7 @@ struct lbm_cuboid {
   bool ghost = false;  // ghost-plane (NCCL) mode
   bool paper_rates = false;  // omega_1 = omega_high = 1 -> k_collide_stream_paper
   bool fd = false;           // FULL_FD: density pass + isotropic gradient
+  bool fd_fused = true;      // FULL_FD: fused 2.5D kernel (env LBM_FD_FUSED=0: two-pass path)
   bool aa = false;           // AA in-place streaming: one buffer; cur = 0 layout R, cur = 1 layout N
   double* d_rho = nullptr;   // FULL_FD density field, population-buffer plane structure (ghost planes)
   cudaEvent_t ev_rho = nullptr;
@@ -166,6 +168,20 @@ int validate(const lbm_cuboid_params* p) {
   const int64_t nxy = int64_t(p->nx) * p->ny;
   if (27 * nxy >= (int64_t(1) << 31)) return fail(LBM_EINVAL, "nx*ny too large (27*nx*ny must fit int32)");
   if (p->nz / p->world > 65535) return fail(LBM_EINVAL, "nz/world must be <= 65535");
+  if (p->corrections != LBM_CORR_OFF) {
+    // the 3x3 strain-rate system of App D at rest must be
+    // regular (a singular system is an error), C / rho at u = 0
+    const double csn = 2.0 * cs2 / p->omega_nu, csx = 2.0 * cs2 / p->omega_xi;
+    const double gx = 3.0 * cs2 - 1.0, gy = 3.0 * cs2 - p->r * p->r, gz = 3.0 * cs2 - p->s * p->s;
+    const double Csx = -csn + 0.5 * gx, Cbx = -csx + 0.5 * gx, Csy = csn - 0.5 * gy, Cby = -csx + 0.5 * gy,
+                 Csz = csn - 0.5 * gz, Cbz = -csx + 0.5 * gz;
+    const double det = -Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx);
+    const double scale = std::max({std::fabs(Csx), std::fabs(Csy), std::fabs(Csz), std::fabs(Cbx), std::fabs(Cby),
+                                   std::fabs(Cbz)});
+    if (!(std::fabs(det) > 1e-12 * scale * scale * scale))
+      return fail(LBM_EINVAL, "the strain-rate system of the corrections is singular at rest (det = %g) for these "
+                  "r, s, cs2, omega_nu, omega_xi", det);
+  }
   return LBM_OK;
 }
 
@@ -312,6 +328,27 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
       LBM_P2P(double);
     else
       LBM_P2P(float);
+  } else if (h->fd && h->fd_fused) {
+    // contiguous planes [zbeg, zbeg + nplanes) in z-chunks; strided single planes otherwise
+    const int zlen = (zstride == 1) ? lbm::kFdZc : 1;
+    const int zst = (zstride == 1) ? lbm::kFdZc : zstride;
+    const int zend = zbeg + (nplanes - 1) * zstride + 1;
+    const int nchunks = (zstride == 1) ? (nplanes + lbm::kFdZc - 1) / lbm::kFdZc : nplanes;
+    const dim3 gf(unsigned((h->p.nx + lbm::kFdTx - 1) / lbm::kFdTx), unsigned((h->p.ny + lbm::kFdTy - 1) / lbm::kFdTy),
+                  unsigned(nchunks));
+    const int kind = (h->p.model == LBM_MODEL_RM) ? lbm::CORE_RAW : (h->paper_rates ? lbm::CORE_PAPER : lbm::CORE_GENERIC);
+#define LBM_FDF(T, K) \
+  lbm::k_collide_stream_fd<T, K><<<gf, lbm::kFdThreads, 0, s>>>((const T*)src, (T*)dst, rf, h->c, zbeg, zst, zlen, zend)
+    if (fp64) {
+      if (kind == lbm::CORE_PAPER) LBM_FDF(double, lbm::CORE_PAPER);
+      else if (kind == lbm::CORE_RAW) LBM_FDF(double, lbm::CORE_RAW);
+      else LBM_FDF(double, lbm::CORE_GENERIC);
+    } else {
+      if (kind == lbm::CORE_PAPER) LBM_FDF(float, lbm::CORE_PAPER);
+      else if (kind == lbm::CORE_RAW) LBM_FDF(float, lbm::CORE_RAW);
+      else LBM_FDF(float, lbm::CORE_GENERIC);
+    }
+#undef LBM_FDF
   } else if (h->p.model == LBM_MODEL_RM)
     LBM_LAUNCH(k_collide_stream_raw);
   else if (h->paper_rates)
@@ -743,13 +780,18 @@ int step_once(lbm_cuboid* h) {
   if (h->aa) return launch_aa(h, h->stream);
   if (h->p2p) return p2p_step(h);
   if (!h->ghost) {
-    if (h->fd && (rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
+    if (h->fd && !h->fd_fused && (rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
     return launch_cs(h, src, dst, 0, h->nzl, 1, h->stream);
   }
   if ((rc = wait_halo(h))) return rc;
   if (h->fd) {
-    // same-time density of every local plane, then its boundary planes to the neighbours
-    if ((rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
+    // same-time density (fused: of the two boundary planes only; the fused
+    // kernel forms the rest itself), then the boundary planes to the neighbours
+    if (h->fd_fused) {
+      if ((rc = launch_density(h, src, 0, (h->nzl > 1) ? 2 : 1, std::max(1, h->nzl - 1), h->stream))) return rc;
+    } else if ((rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) {
+      return rc;
+    }
     if ((rc = exchange_rho(h))) return rc;
   }
   // both boundary planes first, in one launch (critical path of the exchange) ...
@@ -828,6 +870,7 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->peer_down = hp.peer_down;
   h->paper_rates = (p->omega_1 == 1.0 && p->omega_high == 1.0);
   h->fd = (p->corrections == LBM_CORR_FULL_FD);
+  if (const char* e = std::getenv("LBM_FD_FUSED")) h->fd_fused = (std::atoi(e) != 0);
   h->aa = (p->streaming == LBM_STREAM_AA);
   h->p2p = h->ghost && (p->halo == LBM_HALO_P2P);
   fill_consts(h);

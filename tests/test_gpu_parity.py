@@ -572,3 +572,38 @@ def test_persistent_kernel_long_run_chunks_and_oracle(P):
     o.step(1031)
     _cmp(o, g)
     g.close()
+
+
+FD_FUSED_CASES = {
+    # ragged tiles (nx % 32, ny % 8 != 0) and z-chunks (nz % 16 != 0)
+    "tgv_ragged": (synth.CONFIGS["tgv"].scaled(nx=45, ny=13, nz=37), {}),
+    "cavity_lid_walls": (synth.CONFIGS["cavity100"].scaled(nx=33, ny=17, nz=20), {}),
+    "shear_slip_raw_fp32": (synth.CONFIGS["shear"].scaled(nx=40, ny=9, nz=18), {"model": 1, "precision": 1}),
+    "duct_generic": (synth.CONFIGS["duct"].scaled(nx=7, ny=26, nz=17), {"omega_1": 1.3, "omega_high": 0.8}),
+    "thin": (synth.CONFIGS["tgv"].scaled(nx=3, ny=2, nz=2), {}),
+}
+
+
+@pytest.mark.parametrize("case", list(FD_FUSED_CASES))
+def test_full_fd_fused_kernel_bitwise_equal_two_pass(P, case, monkeypatch):
+    """The fused FULL_FD kernel (2.5D tiles, shared-memory density ring) equals
+    the two-pass path (density pass + collide) bit for bit, also through the
+    NCCL ghost-plane path (boundary-plane density exchanged)."""
+    w, kw = FD_FUSED_CASES[case]
+    w = w.scaled(corrections=synth.CORR_FULL_FD)
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 61)
+    monkeypatch.setenv("LBM_FD_FUSED", "0")
+    a = _gpu(P, w, graphs=1, **kw)
+    monkeypatch.setenv("LBM_FD_FUSED", "1")
+    b = _gpu(P, w, graphs=1, **kw)
+    hs = [a, b]
+    if w.bc[4] == synth.BC_PERIODIC:
+        hs.append(_gpu(P, w, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id(), **kw))
+    for g in hs:
+        g.init_fields(rho, u)
+        g.step(23)
+    fa = a.get_populations()
+    for g in hs[1:]:
+        assert np.array_equal(fa, g.get_populations())
+    for g in hs:
+        g.close()
