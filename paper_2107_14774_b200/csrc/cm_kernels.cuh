@@ -995,8 +995,8 @@ struct StoreHalo {
   const Consts* c;
   T* rup;  // up neighbour's ghost plane at this node, or nullptr
   T* rdn;  // down neighbour's ghost plane at this node, or nullptr
-  const T* up_base;
-  const T* dn_base;
+  T* up_base;
+  T* dn_base;
   __device__ __forceinline__ void begin(double) {}
   __device__ __forceinline__ void operator()(int q, double v) const {
     stcs<T>(LBM_CHECK_ST(base, out + q * nxy, *c), v);

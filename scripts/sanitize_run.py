@@ -1,7 +1,9 @@
 #!/usr/bin/env python
-"""Exercise every kernel of liblbm_cuboid.so on small grids (for compute-sanitizer):
-init (host and device), collide-stream (paper-rate, generic, raw; fp64 and fp32),
-all wall kinds, ghost-plane NCCL self-exchange, graphs, macro, pack/unpack, check."""
+"""Exercise every kernel of liblbm_cuboid.so on small grids (for compute-sanitizer
+or the -DLBM_DEBUG_BOUNDS build): init (host and device), collide-stream
+(paper-rate, generic, raw; fp64 and fp32), FULL_FD fused and two-pass, all wall
+kinds, ghost-plane NCCL self-exchange, fused P2P halo (self and two in-process
+slabs), graphs, the persistent kernel, AA, macro, pack/unpack, check."""
 import os
 import sys
 
@@ -29,11 +31,16 @@ for w in cases:
         for model in (0, 1):
             ww = w.scaled(precision=prec, model=model)
             for kw in ({}, {"halo": 1, "nccl_uid": P.nccl_unique_id()}, {"graphs": 2}, {"streaming": 1},
-                       {"streaming": 1, "graphs": 2}):
-                if "halo" in kw and ww.bc[4] != 0:
+                       {"streaming": 1, "graphs": 2}, {"halo": 2}, {"graphs": 3}, {"fd_two_pass": 1}):
+                if kw.get("halo") and ww.bc[4] != 0:
                     continue
-                if "streaming" in kw and ww.corrections == synth.CORR_FULL_FD:
+                if ("streaming" in kw or kw.get("halo") == 2) and ww.corrections == synth.CORR_FULL_FD:
                     continue
+                if "fd_two_pass" in kw:
+                    if ww.corrections != synth.CORR_FULL_FD:
+                        continue
+                    kw = {}
+                    os.environ["LBM_FD_FUSED"] = "0"
                 g = P.Lattice(**ww.params(), **kw)
                 rho, u = synth.random_fields(ww.nx, ww.ny, ww.nz, 5)
                 g.init_fields(rho, u)
@@ -52,5 +59,24 @@ for w in cases:
                 g.timing(False)
                 g.sync()
                 g.close()
+                os.environ.pop("LBM_FD_FUSED", None)
+            # two P2P slabs in this process, stepped one at a time (remote ghost stores)
+            if ww.nz % 2 == 0 and ww.corrections != synth.CORR_FULL_FD:
+                hs = [P.Lattice(**ww.params(), rank=r, world=2, halo=2) for r in range(2)]
+                blobs = [h.p2p_export() for h in hs]
+                for h in hs:
+                    h.p2p_connect(*P.lbm.p2p_neighbour_blobs(P.lbm.halo_plan(h.p), blobs))
+                rho, u = synth.random_fields(ww.nx, ww.ny, ww.nz, 6)
+                n = ww.nz // 2
+                for r, h in enumerate(hs):
+                    h.init_fields(np.ascontiguousarray(rho[r * n:(r + 1) * n]),
+                                  np.ascontiguousarray(u[:, r * n:(r + 1) * n]))
+                    h.sync()
+                for _ in range(5):
+                    for h in hs:
+                        h.step(1)
+                        h.sync()
+                for h in hs:
+                    h.close()
 torch.cuda.synchronize()
 print("sanitize_run: all kernels exercised")
