@@ -21,7 +21,10 @@ VDIR = os.path.join(ROOT, "build", "variants")
 VARIANTS = {
     "base": [],
     "b128m6": ["LBM_MINB=6"],
+    "b128m7": ["LBM_MINB=7"],
     "b128m8": ["LBM_MINB=8"],
+    "b64m12": ["LBM_BLOCK=64", "LBM_MINB=12"],
+    "b64m14": ["LBM_BLOCK=64", "LBM_MINB=14"],
     "b64": ["LBM_BLOCK=64"],
     "b256": ["LBM_BLOCK=256"],
     "b256m3": ["LBM_BLOCK=256", "LBM_MINB=3"],
