@@ -38,8 +38,10 @@
  * and Eq. 69, conservation, SRT limit, analytic TGV/shear-wave/duct decay,
  * viscous and acoustic isotropy, Galilean invariance, moving-frame sound
  * attenuation for the density-gradient terms, Womersley).
- * Parity unpinned: the free-slip rule (reading R7) is not in the paper; it is
- * checked only against invariants (mass and tangential momentum conservation).
+ * The free-slip rule (reading R7) is not in the paper (BASELINE config 4 asks
+ * for it); it is pinned by invariants (mass, tangential momentum) and by the
+ * analytic decay nu k^2 of the cosine shear mode between stress-free walls
+ * (tests/test_oracle_physics.py; bounce-back walls give 8x that rate).
  *
  * Population layout of every array argument: [q][z][y][x], q in the paper's
  * order of Eqs. 1a-1c, x fastest.

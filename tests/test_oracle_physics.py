@@ -170,6 +170,34 @@ def test_free_slip_conserves_mass_and_tangential_momentum():
     assert abs(p1[0] - p0[0]) < 1e-12 * m0 and abs(p1[2] - p0[2]) < 1e-12 * m0
 
 
+@pytest.mark.parametrize("r,s,axis", [(1.0, 2.0, "y"), (0.5, 1.0, "y"), (1.0, 2.0, "z")])
+def test_free_slip_cosine_shear_mode_decay(r, s, axis):
+    """Analytic pin of the free-slip rule (reading R7): between two stress-free
+    walls the shear mode u_x = A cos(n pi (j + 1/2)/N) satisfies du_x/dn = 0 and
+    u_n = 0 at the halfway wall positions j = -1/2 and N - 1/2, so it decays at
+    nu k^2 with k = n pi / (N h), h the node spacing across the walls.  A wrong
+    mirror (e.g. plain bounce-back, or a slip rule that loses tangential
+    momentum) gives a no-slip-like rate for the n = 1 mode (k -> ~2x, rate ~4x)."""
+    nu = 0.05
+    cs2 = synth.auto_cs2(r, s)
+    h = r if axis == "y" else s
+    N = int(round(64.0 / h))
+    FS, PER = synth.BC_FREE_SLIP, synth.BC_PERIODIC
+    bc = (PER, PER, FS, FS, PER, PER) if axis == "y" else (PER, PER, PER, PER, FS, FS)
+    ny, nz = (N, 1) if axis == "y" else (1, N)
+    o = O.Oracle(1, ny, nz, r, s, cs2, synth.omega_from_nu(nu, cs2), bc=bc)
+    for n_mode in (1, 2):
+        k = n_mode * np.pi / (N * h)
+        j = np.arange(N)
+        prof = np.cos(n_mode * np.pi * (j + 0.5) / N)
+        basis = prof.reshape((1, N, 1) if axis == "y" else (N, 1, 1))
+        u = np.zeros((3, nz, ny, 1))
+        u[0] = 1e-4 * basis
+        o.init_fields(np.ones((nz, ny, 1)), u)
+        rate = _decay_rate(o, lambda o: (o.macroscopic()[1][0] * basis).sum(), 20, 300)
+        assert rate / (nu * k * k) == pytest.approx(1.0, abs=0.015), (n_mode, rate / (nu * k * k))
+
+
 def test_periodic_momentum_grows_by_force():
     """Fully periodic: total momentum grows by exactly N F per step (P2)."""
     w = synth.CONFIGS["tgv"].scaled(nx=6, ny=5, nz=4, force=(1e-5, -2e-5, 3e-6))
