@@ -198,6 +198,25 @@ def test_free_slip_cosine_shear_mode_decay(r, s, axis):
         assert rate / (nu * k * k) == pytest.approx(1.0, abs=0.015), (n_mode, rate / (nu * k * k))
 
 
+@pytest.mark.parametrize("r,s", [(1.0, 2.0), (0.5, 1.0), (1.0, 1.0)])
+def test_moving_wall_couette_profile(r, s):
+    """Analytic pin of the moving-wall rule (Eq. 69, readings R4/R5):
+    plane Couette flow between a bounce-back wall at j = -1/2 and the +y lid at
+    j = N - 1/2 moving with U reaches the linear profile u_x = U (j + 1/2)/N.
+    Only du_x/dy is non-zero, so the corrections are inactive and the steady
+    profile is exact up to compressibility (observed <= 6e-5 U)."""
+    nu, N, U = 0.1, 16, 0.05
+    cs2 = synth.auto_cs2(r, s)
+    o = O.Oracle(1, N, 1, r, s, cs2, synth.omega_from_nu(nu, cs2), bc=(0, 0, 1, 2, 0, 0), wall_u=U)
+    o.init_fields(np.ones((1, N, 1)), np.zeros((3, 1, N, 1)))
+    H = N * r
+    o.step(int(12 * H * H / nu))  # slowest mode decays as exp(-nu (pi/H)^2 t): < 1e-40
+    _, u = o.macroscopic()
+    exact = U * (np.arange(N) + 0.5) / N
+    assert np.abs(u[0, 0, :, 0] - exact).max() <= 2e-4 * U
+    assert np.abs(u[1]).max() < 1e-12 and np.abs(u[2]).max() < 1e-12
+
+
 def test_periodic_momentum_grows_by_force():
     """Fully periodic: total momentum grows by exactly N F per step (P2)."""
     w = synth.CONFIGS["tgv"].scaled(nx=6, ny=5, nz=4, force=(1e-5, -2e-5, 3e-6))
