@@ -10,7 +10,9 @@
  * (Eq. LBEcentralmomentcuboidlattice; step list P:L687-742; collision
  * App D) with halfway bounce-back and the momentum-augmented
  * moving wall of Eq. 69, on one GPU or on a z-slab decomposition
- * over several GPUs (one process per GPU, NCCL halo exchange).
+ * over several GPUs (one process per GPU; ghost-plane halo exchanged with NCCL,
+ * or stored by the boundary-plane kernel itself into the neighbours' ghost planes
+ * over NVLink peer memory, LBM_HALO_P2P).
  *
  * Conventions
  *  - Lattice units: dx = dt = 1, dy = r, dz = s.
