@@ -92,6 +92,18 @@ def test_parity_fp64_100_steps(P, name):
     _cmp(o, g)
 
 
+def test_parity_config2_duct_full_size(P):
+    """BASELINE config 2 at its full size (8x128x64, force, walls in y and z),
+    100 steps from non-equilibrium populations, element by element (the oracle
+    needs ~10 s for these 6.6 M node updates)."""
+    w = synth.CONFIGS["duct"]
+    o, g = _init_both(P, w, seed=17, noneq=1e-3)
+    o.step(100)
+    g.step(100)
+    _cmp(o, g)
+    g.close()
+
+
 @pytest.mark.parametrize("name", ["tgv_full", "cavity100", "shear", "duct"])
 def test_parity_fp32_storage(P, name):
     w = CASES[name].scaled(precision=synth.PREC_FP32)
