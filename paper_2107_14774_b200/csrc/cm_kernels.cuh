@@ -277,32 +277,50 @@ __device__ __forceinline__ void collide_generic(const Consts& c, double (&f)[27]
 // -------------------------------------------------------------- streaming
 // Gather the 27 incoming populations of node (x, y, z) (pull form).
 // Fast path: no wall face adjacent -> periodic/ghost addressing only.
+// Pull sources of node (x, y, z): x/y neighbour indices with periodic wrap,
+// the three source planes (ghost planes at -1 / nz_l unless z wraps), and
+// whether a wall face is adjacent (then gather() applies the wall rules).
+template <typename T>
+struct PullSrc {
+  int sx[3], sy[3];  // source x, y*nx for displacement e + 1 (source = node - e)
+  const T* pz[3];    // source plane for e_z + 1
+  bool wall;
+  __device__ __forceinline__ PullSrc(const T* src, const Consts& c, int x, int y, int z) {
+    const int nx = c.nx;
+    const int xm = (x == 0) ? nx - 1 : x - 1;        // source of e_x = +1
+    const int xp = (x == nx - 1) ? 0 : x + 1;        // source of e_x = -1
+    const int ym = (y == 0) ? c.ny - 1 : y - 1;
+    const int yp = (y == c.ny - 1) ? 0 : y + 1;
+    int zm = z - 1, zp = z + 1;                      // -1 / nz_l address ghost planes
+    if (z == 0 && c.face[4] == FK_WRAP) zm = c.nzl - 1;
+    if (z == c.nzl - 1 && c.face[5] == FK_WRAP) zp = 0;
+    sx[0] = xp; sx[1] = x; sx[2] = xm;
+    sy[0] = yp * nx; sy[1] = y * nx; sy[2] = ym * nx;
+    pz[0] = src + (long long)(zp + 1) * c.plane;
+    pz[1] = src + (long long)(z + 1) * c.plane;
+    pz[2] = src + (long long)(zm + 1) * c.plane;
+    wall = false;
+    if (c.has_walls) {
+      wall = (x == 0 && c.face[0] >= FK_BOUNCE && c.face[0] <= FK_SLIP) ||
+             (x == nx - 1 && c.face[1] >= FK_BOUNCE && c.face[1] <= FK_SLIP) ||
+             (y == 0 && c.face[2] >= FK_BOUNCE && c.face[2] <= FK_SLIP) ||
+             (y == c.ny - 1 && c.face[3] >= FK_BOUNCE && c.face[3] <= FK_SLIP) ||
+             (z == 0 && c.face[4] >= FK_BOUNCE && c.face[4] <= FK_SLIP) ||
+             (z == c.nzl - 1 && c.face[5] >= FK_BOUNCE && c.face[5] <= FK_SLIP);
+    }
+  }
+};
+
 // REV (AA odd steps): the source buffer holds f~_s(z) at slot 26 - s of node z.
 template <typename T, bool REV = false>
 __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int y, int z, double (&f)[27]) {
   auto slot = [](int s) { return REV ? 26 - s : s; };
   const int nx = c.nx;
-  const int xm = (x == 0) ? nx - 1 : x - 1;        // source of e_x = +1
-  const int xp = (x == nx - 1) ? 0 : x + 1;        // source of e_x = -1
-  const int ym = (y == 0) ? c.ny - 1 : y - 1;
-  const int yp = (y == c.ny - 1) ? 0 : y + 1;
-  int zm = z - 1, zp = z + 1;                      // -1 / nz_l address ghost planes
-  if (z == 0 && c.face[4] == FK_WRAP) zm = c.nzl - 1;
-  if (z == c.nzl - 1 && c.face[5] == FK_WRAP) zp = 0;
-  const int sx[3] = {xp, x, xm};                   // index by e + 1
-  const int sy[3] = {yp * nx, y * nx, ym * nx};
-  const T* pz[3] = {src + (long long)(zp + 1) * c.plane, src + (long long)(z + 1) * c.plane,
-                    src + (long long)(zm + 1) * c.plane};
-
-  bool wall = false;
-  if (c.has_walls) {
-    wall = (x == 0 && c.face[0] >= FK_BOUNCE && c.face[0] <= FK_SLIP) ||
-           (x == nx - 1 && c.face[1] >= FK_BOUNCE && c.face[1] <= FK_SLIP) ||
-           (y == 0 && c.face[2] >= FK_BOUNCE && c.face[2] <= FK_SLIP) ||
-           (y == c.ny - 1 && c.face[3] >= FK_BOUNCE && c.face[3] <= FK_SLIP) ||
-           (z == 0 && c.face[4] >= FK_BOUNCE && c.face[4] <= FK_SLIP) ||
-           (z == c.nzl - 1 && c.face[5] >= FK_BOUNCE && c.face[5] <= FK_SLIP);
-  }
+  const PullSrc<T> ps(src, c, x, y, z);
+  const int* sx = ps.sx;
+  const int* sy = ps.sy;
+  const T* const* pz = ps.pz;
+  const bool wall = ps.wall;
   if (!wall) {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
@@ -924,7 +942,8 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T*
 }
 
 // chunk blockIdx.z covers planes [z0, z1), z0 = zbeg + blockIdx.z * zstride,
-// z1 = min(z0 + zlen, zend)
+// z1 = min(z0 + zlen, zend).  Iteration p forms rho(p) on the tile and its ring,
+// then collides plane p - 1.
 template <typename T, int KIND>
 __device__ __forceinline__ void collide_stream_fd_fused(const T* __restrict__ src, T* __restrict__ dst,
                                                         const double* __restrict__ rf, const Consts& c, int zbeg,

@@ -12,13 +12,12 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "build", "fd_variants")
 VARIANTS = {
-    "zc32_ty4": ["LBM_FD_ZC=32", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
-    "zc16_ty4": ["LBM_FD_ZC=16", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
-    "zc64_ty4": ["LBM_FD_ZC=64", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
-    "zc32_ty2": ["LBM_FD_ZC=32", "LBM_FD_TY=2", "LBM_FD_MINB=8"],
-    "zc32_tx64_ty2": ["LBM_FD_ZC=32", "LBM_FD_TX=64", "LBM_FD_TY=2", "LBM_FD_MINB=4"],
-    "zc32_tx64_ty4": ["LBM_FD_ZC=32", "LBM_FD_TX=64", "LBM_FD_TY=4", "LBM_FD_MINB=2"],
-    "zc32_ty1": ["LBM_FD_ZC=32", "LBM_FD_TY=1", "LBM_FD_MINB=16"],
+    "sync_zc32_ty4": ["LBM_FD_ASYNC=0", "LBM_FD_ZC=32", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
+    "async_zc32_ty4": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=32", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
+    "async_zc32_ty4_m3": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=32", "LBM_FD_TY=4", "LBM_FD_MINB=3"],
+    "async_zc32_ty2": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=32", "LBM_FD_TY=2", "LBM_FD_MINB=6"],
+    "async_zc32_ty8": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=32", "LBM_FD_TY=8", "LBM_FD_MINB=1"],
+    "async_zc64_ty4": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=64", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
 }
 
 if sys.argv[1] == "build":
