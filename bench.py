@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["cuda", "reference"], default="cuda")
-    ap.add_argument("--workload", default="weak", choices=["weak", "strong", "shear", "cavity100", "cavity1000", "tgv"])
+    ap.add_argument("--workload", default="weak", choices=["weak", "strong", "shear", "cavity100", "cavity1000", "tgv", "duct"])
     ap.add_argument("--streaming", choices=["ab", "aa"], default="ab",
                     help="aa: one population buffer updated in place (single GPU)")
     ap.add_argument("--precision", choices=["fp64", "fp32"], default="fp64")
