@@ -320,7 +320,10 @@ __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int
   const int* sx = ps.sx;
   const int* sy = ps.sy;
   const T* const* pz = ps.pz;
-  const bool wall = ps.wall;
+  // warp-uniform choice: a warp with any wall-adjacent lane takes the wall path
+  // (which reduces to the plain pull for its other lanes) instead of running
+  // both paths one after the other
+  const bool wall = __any_sync(__activemask(), ps.wall);
   if (!wall) {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
@@ -359,22 +362,23 @@ __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int
         const int kz = ez > 0 ? czp : (ez < 0 ? czm : 0);
         const bool noslip = (kx == FK_BOUNCE || kx == FK_MOVING) || (ky == FK_BOUNCE || ky == FK_MOVING) ||
                             (kz == FK_BOUNCE || kz == FK_MOVING);
-        if (noslip) {
-          // halfway bounce-back from the own node's opposite direction
-          double v = ldg(LBM_CHECK_LD(src, p0 + slot(LBM_Q(2 - i, 2 - j, 2 - k)) * c.nxy + own, c));
-          if (ky == FK_MOVING)  // Eq. 69: + rho_f U e_x cs2/(2 r^2) phi_z(e_z)
-            v = fma(rho_f * c.lid_u * (double)ex, c.lid_c[k], v);
-          f[q] = v;
-        } else {
-          // free-slip (reading R7): mirror the crossed axes, source at the own
-          // coordinate along them; otherwise the periodic/ghost neighbour
-          const bool mx = (kx == FK_SLIP), my = (ky == FK_SLIP), mz = (kz == FK_SLIP);
-          const int qi = mx ? 2 - i : i, qj = my ? 2 - j : j, qk = mz ? 2 - k : k;
-          const int xs = mx ? x : sx[i];
-          const int ys = my ? y * nx : sy[j];
-          const T* zs = mz ? p0 : pz[k];
-          f[q] = ldg(LBM_CHECK_LD(src, zs + slot(LBM_Q(qi, qj, qk)) * c.nxy + ys + xs, c));
-        }
+        // one load per direction, its source chosen per lane:
+        //  no-slip crossing: halfway bounce-back from the own node's opposite
+        //    direction, plus the Eq. 69 term across the lid;
+        //  free-slip crossing (reading R7): the crossed axes mirrored, source at
+        //    the own coordinate along them;
+        //  otherwise the periodic/ghost neighbour
+        const bool mx = (kx == FK_SLIP), my = (ky == FK_SLIP), mz = (kz == FK_SLIP);
+        const int qi = mx ? 2 - i : i, qj = my ? 2 - j : j, qk = mz ? 2 - k : k;
+        const int xs = mx ? x : sx[i];
+        const int ys = my ? y * nx : sy[j];
+        const T* zs = mz ? p0 : pz[k];
+        const T* a_slip = zs + slot(LBM_Q(qi, qj, qk)) * c.nxy + ys + xs;
+        const T* a_bb = p0 + slot(LBM_Q(2 - i, 2 - j, 2 - k)) * c.nxy + own;
+        double v = ldg(LBM_CHECK_LD(src, noslip ? a_bb : a_slip, c));
+        if (ky == FK_MOVING)  // Eq. 69: + rho_f U e_x cs2/(2 r^2) phi_z(e_z)
+          v = fma(rho_f * c.lid_u * (double)ex, c.lid_c[k], v);
+        f[q] = v;
       }
 }
 
