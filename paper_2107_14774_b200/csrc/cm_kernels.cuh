@@ -570,7 +570,9 @@ struct StorePush {
     cz[0] = (z == 0) ? kind(cc.face[4]) : 0;
     cz[1] = 0;
     cz[2] = (z == cc.nzl - 1) ? kind(cc.face[5]) : 0;
-    wall = cx[0] | cx[2] | cy[0] | cy[2] | cz[0] | cz[2];
+    // warp-uniform: a warp with any wall-adjacent lane stores through the wall
+    // rules (which reduce to the plain push for its other lanes)
+    wall = __any_sync(__activemask(), (cx[0] | cx[2] | cy[0] | cy[2] | cz[0] | cz[2]) != 0);
     rho_f = 0.0;
   }
   __device__ __forceinline__ void begin(double rho) { rho_f = rho; }
@@ -584,19 +586,21 @@ struct StorePush {
     const int kx = cx[i], ky = cy[j], kz = cz[k];
     const bool noslip = (kx == FK_BOUNCE || kx == FK_MOVING) || (ky == FK_BOUNCE || ky == FK_MOVING) ||
                         (kz == FK_BOUNCE || kz == FK_MOVING);
-    if (noslip) {
-      double w = v;
-      if (ky == FK_MOVING)  // arrives as direction 26 - q: + rho_f U e_x(26-q) lid_c[e_z(26-q)]
-        w = fma(rho_f * c->lid_u * (double)(1 - i), c->lid_c[2 - k], w);
-      stcs<T>(LBM_CHECK_ST(base, pz[1] + (26 - q) * nxy + own, *c), w);
-    } else {
-      const bool mx = (kx == FK_SLIP), my = (ky == FK_SLIP), mz = (kz == FK_SLIP);
-      const int qi = mx ? 2 - i : i, qj = my ? 2 - j : j, qk = mz ? 2 - k : k;
-      const int xs = mx ? x : dx[i];
-      const int ys = my ? y * c->nx : dy[j];
-      T* zs = mz ? pz[1] : pz[k];
-      stcs<T>(LBM_CHECK_ST(base, zs + LBM_Q(qi, qj, qk) * nxy + ys + xs, *c), v);
-    }
+    // one store per direction, its destination chosen per lane: a crossed no-slip
+    // face -> own node slot 26 - q (+ the Eq. 69 term across the lid, arriving as
+    // direction 26 - q: + rho_f U e_x(26-q) lid_c[e_z(26-q)]); a crossed
+    // free-slip face -> mirrored slot at the own coordinate along the crossed
+    // axes; otherwise the periodic neighbour
+    const bool mx = (kx == FK_SLIP), my = (ky == FK_SLIP), mz = (kz == FK_SLIP);
+    const int qi = mx ? 2 - i : i, qj = my ? 2 - j : j, qk = mz ? 2 - k : k;
+    const int xs = mx ? x : dx[i];
+    const int ys = my ? y * c->nx : dy[j];
+    T* zs = mz ? pz[1] : pz[k];
+    T* a_slip = zs + LBM_Q(qi, qj, qk) * nxy + ys + xs;
+    T* a_bb = pz[1] + (26 - q) * nxy + own;
+    double w = v;
+    if (ky == FK_MOVING) w = fma(rho_f * c->lid_u * (double)(1 - i), c->lid_c[2 - k], w);
+    stcs<T>(LBM_CHECK_ST(base, noslip ? a_bb : a_slip, *c), w);
   }
 };
 

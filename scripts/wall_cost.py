@@ -31,12 +31,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--precision", default="fp64")
     ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--streaming", choices=["ab", "aa"], default="ab")
+    ap.add_argument("--case", default=None, help="run only the cases whose name starts with this")
     args = ap.parse_args()
     prec = 0 if args.precision == "fp64" else 1
     base = synth.CONFIGS["cavity100"].scaled(precision=prec)
     for name, bc in CASES.items():
+        if args.case and not name.startswith(args.case):
+            continue
         w = base.scaled(bc=bc)
-        lat = P.Lattice(device=0, graphs=1, **w.params())
+        lat = P.Lattice(device=0, graphs=1, streaming=1 if args.streaming == "aa" else 0, **w.params())
         rho, u = synth.rest_fields(w.nx, w.ny, w.nz)
         lat.init_fields(rho, u)
         lat.step(20)
@@ -47,7 +51,7 @@ def main():
         b.record(lat.stream)
         lat.sync()
         ms = a.elapsed_time(b) / args.steps
-        print(json.dumps({"case": name, "precision": args.precision, "ms_per_step": ms,
+        print(json.dumps({"case": name, "precision": args.precision, "streaming": args.streaming, "ms_per_step": ms,
                           "mlups": w.nodes / ms / 1e3}), flush=True)
         lat.close()
 
