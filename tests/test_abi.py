@@ -102,3 +102,29 @@ def test_c_example_compiles_against_the_header(P, tmp_path):
                            "-L", os.path.dirname(P.lbm.LIB_PATH), "-l:liblbm_cuboid.so",
                            f"-Wl,-rpath,{os.path.dirname(P.lbm.LIB_PATH)}", "-lm"])
     assert exe.exists()
+
+
+def test_params_struct_layout_matches_header(P, tmp_path):
+    """The ctypes mirror of lbm_cuboid_params has the C struct's size and field
+    offsets (gcc, from include/lbm_cuboid.h); LBM_P2P_BLOB_BYTES agrees."""
+    fields = [f[0] for f in P.lbm.Params._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text("#include <stddef.h>\n#include <stdio.h>\n#include \"lbm_cuboid.h\"\nint main(void) {\n"
+                   "  printf(\"size %zu\\n\", sizeof(lbm_cuboid_params));\n"
+                   "  printf(\"blob %d\\n\", LBM_P2P_BLOB_BYTES);\n"
+                   + "".join(f"  printf(\"{f} %zu\\n\", offsetof(lbm_cuboid_params, {f}));\n" for f in fields)
+                   + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-std=c99", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = dict(line.split() for line in subprocess.check_output([str(exe)], text=True).splitlines())
+    import ctypes
+
+    assert int(out.pop("size")) == ctypes.sizeof(P.lbm.Params)
+    assert int(out.pop("blob")) == P.lbm.P2P_BLOB_BYTES
+    for f in fields:
+        assert int(out[f]) == getattr(P.lbm.Params, f).offset, f
+    # every field of the C struct is mirrored (count the declarators in the header)
+    hdr = re.sub(r"/\*.*?\*/", "", open(HDR).read(), flags=re.S)
+    body = hdr[hdr.index("typedef struct {"):hdr.index("} lbm_cuboid_params;")]
+    names = re.findall(r"[\s*](\w+)\s*(?:\[\d+\])?\s*[,;]", body)
+    assert sorted(names) == sorted(fields), (sorted(names), sorted(fields))
