@@ -241,3 +241,23 @@ def test_p2p_cuda_ipc_between_processes(P, world, case):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=240, cwd=root)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert '"bitwise_equal": true' in r.stdout, r.stdout
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_config5_geometry_64cubed_slabs_bitwise(P, world):
+    """1 vs 2/4/8 ranks on 64x64x64 bitwise-equal (config 5
+    physics: periodic TGV, r = 1, s = 2, nu = 0.01), 30 steps, P2P slabs."""
+    w = synth.CONFIGS["weak"].scaled(nx=64, ny=64, nz=64)
+    rho, u = synth.initial_fields(w)
+    ref = _lat(P, w)
+    ref.init_fields(rho, u)
+    ref.step(30)
+    f_ref = ref.get_populations()
+    ref.close()
+    hs = _slabs(P, w, world)
+    _split_init(hs, rho, u)
+    for _ in range(30):
+        _serial(hs, lambda h: h.step(1))
+    f = _gather(hs)
+    _close(hs)
+    assert np.array_equal(f, f_ref)
