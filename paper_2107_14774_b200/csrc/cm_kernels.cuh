@@ -49,6 +49,7 @@ struct Consts {
   long long plane;      // 27 * nxy elements
   int face[6];          // FaceKind per local face -x,+x,-y,+y,-z,+z
   int has_walls;        // any face is BOUNCE/MOVING/SLIP
+  int has_slip;         // any face is SLIP
   int corr_on;          // corrections != OFF
   double r, s, cs2;
   double h1y, h2y, h1z, h2z;  // 1/(2r), 1/(2r^2), 1/(2s), 1/(2s^2)
@@ -348,6 +349,28 @@ __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int
   if (cym == FK_MOVING) {
 #pragma unroll
     for (int q = 0; q < 27; ++q) rho_f += ldg(LBM_CHECK_LD(src, p0 + q * c.nxy + own, c));
+  }
+  if (!c.has_slip) {
+    // no free-slip face (uniform branch): per direction either the plain pull or
+    // the halfway bounce-back source (+ the Eq. 69 term across the lid)
+    const bool nx0 = cxm != 0, nx2 = cxp != 0, ny0 = cym != 0, ny2 = cyp != 0, nz0 = czm != 0, nz2 = czp != 0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int q = LBM_Q(i, j, k);
+          const bool noslip = (i == 0 ? nx0 : (i == 2 ? nx2 : false)) || (j == 0 ? ny0 : (j == 2 ? ny2 : false)) ||
+                              (k == 0 ? nz0 : (k == 2 ? nz2 : false));
+          const T* a_plain = pz[k] + slot(q) * c.nxy + sy[j] + sx[i];
+          const T* a_bb = p0 + slot(LBM_Q(2 - i, 2 - j, 2 - k)) * c.nxy + own;
+          double v = ldg(LBM_CHECK_LD(src, noslip ? a_bb : a_plain, c));
+          if (j == 0 && cym == FK_MOVING)  // e_y = -1 crosses the +y lid: Eq. 69
+            v = fma(rho_f * c.lid_u * (double)(i - 1), c.lid_c[k], v);
+          f[q] = v;
+        }
+    return;
   }
 #pragma unroll
   for (int k = 0; k < 3; ++k)

@@ -254,6 +254,9 @@ void fill_consts(lbm_cuboid* h) {
     ph[d][2] = cs2 / (2.0 * cc[d]);
   }
   c.has_walls = 0;
+  c.has_slip = 0;
+  for (int f = 0; f < 6; ++f)
+    if (c.face[f] == lbm::FK_SLIP) c.has_slip = 1;
   for (int f = 0; f < 6; ++f)
     if (c.face[f] >= lbm::FK_BOUNCE && c.face[f] <= lbm::FK_SLIP) c.has_walls = 1;
 }
