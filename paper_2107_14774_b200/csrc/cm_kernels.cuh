@@ -607,6 +607,14 @@ struct StorePush {
       return;
     }
     const int kx = cx[i], ky = cy[j], kz = cz[k];
+    T* a_bb = pz[1] + (26 - q) * nxy + own;
+    double w = v;
+    if (ky == FK_MOVING) w = fma(rho_f * c->lid_u * (double)(1 - i), c->lid_c[2 - k], w);
+    if (!c->has_slip) {  // no free-slip face (uniform): plain push or bounce-back slot
+      const bool noslip = (kx | ky | kz) != 0;
+      stcs<T>(LBM_CHECK_ST(base, noslip ? a_bb : pz[k] + q * nxy + dy[j] + dx[i], *c), w);
+      return;
+    }
     const bool noslip = (kx == FK_BOUNCE || kx == FK_MOVING) || (ky == FK_BOUNCE || ky == FK_MOVING) ||
                         (kz == FK_BOUNCE || kz == FK_MOVING);
     // one store per direction, its destination chosen per lane: a crossed no-slip
@@ -620,9 +628,6 @@ struct StorePush {
     const int ys = my ? y * c->nx : dy[j];
     T* zs = mz ? pz[1] : pz[k];
     T* a_slip = zs + LBM_Q(qi, qj, qk) * nxy + ys + xs;
-    T* a_bb = pz[1] + (26 - q) * nxy + own;
-    double w = v;
-    if (ky == FK_MOVING) w = fma(rho_f * c->lid_u * (double)(1 - i), c->lid_c[2 - k], w);
     stcs<T>(LBM_CHECK_ST(base, noslip ? a_bb : a_slip, *c), w);
   }
 };
