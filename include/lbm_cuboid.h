@@ -100,7 +100,9 @@ typedef enum {
                         and publishes a per-step epoch flag; the neighbour's stream waits on the
                         flag (no NCCL, no spinning kernel).  The boundary planes run on a second,
                         high-priority stream concurrently with the interior.  Requires
-                        lbm_cuboid_p2p_connect() when world > 1; not with LBM_CORR_FULL_FD or AA. */
+                        lbm_cuboid_p2p_connect() when world > 1; not with AA streaming.  With
+                        LBM_CORR_FULL_FD a density kernel first pushes the boundary planes'
+                        density into the neighbours' density ghost planes (a second epoch). */
 } lbm_halo;
 
 /* Size of the opaque blob lbm_cuboid_p2p_export() writes. */
@@ -174,7 +176,10 @@ int lbm_cuboid_halo_plan(const lbm_cuboid_params *p, int64_t out[8]);
  * the peer mapping fails.  Handles of one process (e.g. several ranks' slabs
  * driven from one thread) are connected with direct pointers.  The neighbours
  * must stay alive until this handle is destroyed (destroy waits, up to 30 s,
- * for the neighbours' last epoch so no peer store is in flight). */
+ * for the neighbours' last epoch so no peer store is in flight).  Ranks must
+ * step concurrently (one process or thread per rank): a step waits for the
+ * neighbours' previous step, and with LBM_CORR_FULL_FD also for their
+ * boundary-plane density of the same step. */
 int lbm_cuboid_p2p_export(const lbm_cuboid_t *h, void *blob);
 int lbm_cuboid_p2p_connect(lbm_cuboid_t *h, const void *blob_down, const void *blob_up);
 

@@ -1082,15 +1082,17 @@ __device__ __forceinline__ void p2p_signal(const P2PArgs<T>& a) {
   }
 }
 
-template <typename T, int KIND>
+template <typename T, int KIND, bool FD>
 __global__ void LBM_CS_BOUNDS k_collide_stream_p2p(const T* __restrict__ src, T* __restrict__ dst,
-                                                   const __grid_constant__ Consts c, int zbeg, int zstride,
-                                                   const P2PArgs<T> a) {
+                                                   const double* __restrict__ rf, const __grid_constant__ Consts c,
+                                                   int zbeg, int zstride, const P2PArgs<T> a) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx < c.nxy) {  // no early return: every thread reaches the barrier of p2p_signal
     const int y = idx / c.nx;
     const int x = idx - y * c.nx;
     const int z = zbeg + blockIdx.y * zstride;
+    double gxr = 0.0, gyr = 0.0, gzr = 0.0;
+    if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);  // ghost-plane rho pushed by the neighbours
     double f[27];
     gather<T>(src, c, x, y, z, f);
     StoreHalo<T> st{dst,
@@ -1101,7 +1103,36 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_p2p(const T* __restrict__ src, T*
                     (z == 0 && a.dn) ? a.dn + (long long)(c.nzl + 1) * c.plane + idx : nullptr,
                     a.up,
                     a.dn};
-    run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, st);
+    run_core<KIND, FD>(c, f, gxr, gyr, gzr, st);
+  }
+  p2p_signal(a);
+}
+
+// FULL_FD with the P2P halo: the same-time density (as k_density) of the
+// planes the boundary-plane collision reads, planes = {0, 1, nz_l-2, nz_l-1}
+// (blockIdx.y indexes the list), the two boundary planes' also stored into
+// the neighbours' density ghost planes (a.up / a.dn are the neighbours'
+// density fields), then signal.
+struct PlaneList {
+  int z[4];
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_density_p2p(const T* __restrict__ src, double* __restrict__ rho_out,
+                                                        const __grid_constant__ Consts c, const PlaneList pl,
+                                                        const P2PArgs<double> a) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx < c.nxy) {
+    const int y = idx / c.nx;
+    const int z = pl.z[blockIdx.y];
+    double f[27];
+    gather<T>(src, c, idx - y * c.nx, y, z, f);
+    double r0 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 27; ++q) r0 += f[q];
+    rho_out[(long long)(z + 1) * c.nxy + idx] = r0;
+    if (z == c.nzl - 1 && a.up) a.up[idx] = r0;                                     // up's ghost p = 0
+    if (z == 0 && a.dn) a.dn[(long long)(c.nzl + 1) * c.nxy + idx] = r0;           // down's ghost p = nz_l + 1
   }
   p2p_signal(a);
 }

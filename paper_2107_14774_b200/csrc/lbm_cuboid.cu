@@ -99,6 +99,8 @@ struct lbm_cuboid {
   unsigned int* d_sig = nullptr;  // [0] epoch from the down neighbour, [1] from the up one, [2] CTA counter
   void* peer_buf_up[2] = {nullptr, nullptr};  // neighbours' population buffers, mapped
   void* peer_buf_dn[2] = {nullptr, nullptr};
+  double* peer_rho_up = nullptr;         // neighbours' FULL_FD density fields, mapped
+  double* peer_rho_dn = nullptr;
   unsigned int* peer_flag_up = nullptr;  // my slot in the up neighbour's flag words ([0])
   unsigned int* peer_flag_dn = nullptr;  // my slot in the down neighbour's flag words ([1])
   std::vector<void*> ipc_open;           // IPC mappings to close
@@ -151,8 +153,6 @@ int validate(const lbm_cuboid_params* p) {
   if (p->corrections < 0 || p->corrections > 3) return fail(LBM_EINVAL, "corrections must be an lbm_corr");
   if (p->precision < 0 || p->precision > 1) return fail(LBM_EINVAL, "precision must be an lbm_prec");
   if (p->halo < 0 || p->halo > 2) return fail(LBM_EINVAL, "halo must be an lbm_halo");
-  if (p->halo == LBM_HALO_P2P && p->corrections == LBM_CORR_FULL_FD)
-    return fail(LBM_ENOTSUP, "LBM_HALO_P2P does not support FULL_FD (use LBM_HALO_NCCL)");
   if (p->graphs < 0 || p->graphs > 3) return fail(LBM_EINVAL, "graphs must be 0, 1, 2 or 3");
   if (p->model < 0 || p->model > 1) return fail(LBM_EINVAL, "model must be an lbm_model");
   if (p->streaming < 0 || p->streaming > 1) return fail(LBM_EINVAL, "streaming must be an lbm_streaming");
@@ -316,15 +316,22 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
 #define LBM_P2P(T)                                                                                           \
   do {                                                                                                       \
     const lbm::P2PArgs<T> a = p2p_args<T>(h, p2p_which, p2p_epoch);                                          \
-    if (h->p.model == LBM_MODEL_RM)                                                                          \
-      lbm::k_collide_stream_p2p<T, lbm::CORE_RAW><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, h->c, zbeg, \
-                                                                            zstride, a);                     \
-    else if (h->paper_rates)                                                                                 \
-      lbm::k_collide_stream_p2p<T, lbm::CORE_PAPER><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, h->c,  \
-                                                                              zbeg, zstride, a);             \
+    if (h->fd)                                                                                               \
+      LBM_P2PK(T, true, a);                                                                                  \
     else                                                                                                     \
-      lbm::k_collide_stream_p2p<T, lbm::CORE_GENERIC><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, h->c, \
-                                                                                zbeg, zstride, a);           \
+      LBM_P2PK(T, false, a);                                                                                 \
+  } while (0)
+#define LBM_P2PK(T, FD, a)                                                                                   \
+  do {                                                                                                       \
+    if (h->p.model == LBM_MODEL_RM)                                                                          \
+      lbm::k_collide_stream_p2p<T, lbm::CORE_RAW, FD><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, rf,  \
+                                                                                h->c, zbeg, zstride, a);     \
+    else if (h->paper_rates)                                                                                 \
+      lbm::k_collide_stream_p2p<T, lbm::CORE_PAPER, FD><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, rf, \
+                                                                                  h->c, zbeg, zstride, a);   \
+    else                                                                                                     \
+      lbm::k_collide_stream_p2p<T, lbm::CORE_GENERIC, FD><<<g, lbm::kBlock, 0, s>>>(                         \
+          (const T*)src, (T*)dst, rf, h->c, zbeg, zstride, a);                                               \
   } while (0)
   if (p2p_which >= 0) {
     if (fp64)
@@ -360,6 +367,7 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
     LBM_LAUNCH(k_collide_stream);
 #undef LBM_LAUNCH
 #undef LBM_P2P
+#undef LBM_P2PK
   CU(cudaGetLastError());
   if (timed) {
     CU(cudaEventRecord(h->ev_t.back().second, s));
@@ -632,9 +640,9 @@ struct P2PBlob {
   char magic[8];
   int32_t pid, device, rank, world, precision, nx, ny, nzl, ipc_ok, pad;
   int64_t buf_elems;
-  uint64_t ptr[3];   // buffer 0, buffer 1, flag words (addresses in the exporting process)
-  uint64_t off[3];   // offset of ptr[i] from the base of its allocation
-  cudaIpcMemHandle_t ipc[3];
+  uint64_t ptr[4];   // buffer 0, buffer 1, flag words, FULL_FD density field or 0 (exporter's addresses)
+  uint64_t off[4];   // offset of ptr[i] from the base of its allocation
+  cudaIpcMemHandle_t ipc[4];
 };
 static_assert(sizeof(P2PBlob) <= LBM_P2P_BLOB_BYTES, "P2P blob too large");
 constexpr char kBlobMagic[8] = {'L', 'B', 'M', 'P', '2', 'P', '1', 0};
@@ -715,6 +723,36 @@ int p2p_step(lbm_cuboid* h) {
   }
   if ((rc = p2p_fork(h)) || (rc = p2p_wait(h))) return rc;
   const int nb = (h->nzl > 1) ? 2 : 1;
+  if (h->fd) {
+    // FULL_FD: publish the same-time density of the boundary planes into the
+    // neighbours' density ghost planes first, then wait for theirs
+    // planes the boundary-plane collision needs: 0, 1, nz_l - 2, nz_l - 1 (distinct)
+    lbm::PlaneList pl{};
+    int np = 0;
+    for (int z : {0, 1, h->nzl - 2, h->nzl - 1}) {
+      bool seen = (z < 0 || z >= h->nzl);
+      for (int i = 0; i < np; ++i) seen = seen || (pl.z[i] == z);
+      if (!seen) pl.z[np++] = z;
+    }
+    const dim3 gd = grid_for(h, np);
+    lbm::P2PArgs<double> ra;
+    ra.up = h->peer_rho_up;
+    ra.dn = h->peer_rho_dn;
+    ra.counter = h->d_sig + 2;
+    ra.flag_up = h->peer_flag_up;
+    ra.flag_dn = h->peer_flag_dn;
+    ra.epoch = h->epoch + 1;
+    if (h->p.precision == LBM_FP64)
+      lbm::k_density_p2p<double><<<gd, lbm::kBlock, 0, h->comm_stream>>>((const double*)src, h->d_rho, h->c, pl,
+                                                                          ra);
+    else
+      lbm::k_density_p2p<float><<<gd, lbm::kBlock, 0, h->comm_stream>>>((const float*)src, h->d_rho, h->c, pl,
+                                                                         ra);
+    CU(cudaGetLastError());
+    h->launches++;
+    h->epoch++;
+    if ((rc = p2p_wait(h))) return rc;
+  }
   if ((rc = launch_cs(h, src, dst, 0, nb, std::max(1, h->nzl - 1), h->comm_stream, which, h->epoch + 1, false)))
     return rc;
   h->epoch++;
@@ -1221,8 +1259,9 @@ int lbm_cuboid_p2p_export(const lbm_cuboid_t* h, void* blob) {
   b.nzl = h->nzl;
   b.buf_elems = h->buf_elems;
   b.ipc_ok = 1;
-  void* const ptrs[3] = {h->buf[0], h->buf[1], h->d_sig};
-  for (int i = 0; i < 3; ++i) {
+  void* const ptrs[4] = {h->buf[0], h->buf[1], h->d_sig, h->d_rho};
+  for (int i = 0; i < 4; ++i) {
+    if (!ptrs[i]) continue;  // no density field (not FULL_FD)
     b.ptr[i] = (uint64_t)(uintptr_t)ptrs[i];
     CUdeviceptr base = 0;
     size_t size = 0;
@@ -1264,15 +1303,16 @@ int lbm_cuboid_p2p_connect(lbm_cuboid_t* h, const void* blob_down, const void* b
     if (x.nx != h->p.nx || x.ny != h->p.ny || x.nzl != h->nzl || x.precision != h->p.precision ||
         x.buf_elems != h->buf_elems)
       return fail(LBM_EINVAL, "neighbour blob has another geometry or precision");
+    if ((x.ptr[3] != 0) != h->fd) return fail(LBM_EINVAL, "neighbour blob has another correction mode");
   }
   // map (a rank that is both neighbours is mapped once)
-  void* m[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  void* m[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
   const pid_t me = getpid();
   for (int side = 0; side < 2; ++side) {
     if (peers[side] < 0) continue;
     const P2PBlob& x = b[side];
     if (side == 1 && peers[0] >= 0 && b[0].pid == x.pid && b[0].ptr[0] == x.ptr[0] && b[0].ptr[2] == x.ptr[2]) {
-      for (int i = 0; i < 3; ++i) m[1][i] = m[0][i];
+      for (int i = 0; i < 4; ++i) m[1][i] = m[0][i];
       continue;
     }
     if (x.pid == int32_t(me)) {  // same process: direct pointers (peer access if another device)
@@ -1284,10 +1324,11 @@ int lbm_cuboid_p2p_connect(lbm_cuboid_t* h, const void* blob_down, const void* b
         if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CU(e);
         cudaGetLastError();
       }
-      for (int i = 0; i < 3; ++i) m[side][i] = (void*)(uintptr_t)x.ptr[i];
+      for (int i = 0; i < 4; ++i) m[side][i] = (void*)(uintptr_t)x.ptr[i];
     } else {
       if (!x.ipc_ok) return fail(LBM_EINVAL, "the neighbour's buffers cannot be shared between processes (no IPC)");
-      for (int i = 0; i < 3; ++i) {
+      for (int i = 0; i < 4; ++i) {
+        if (!x.ptr[i]) continue;
         void* base = nullptr;
         CU(cudaIpcOpenMemHandle(&base, x.ipc[i], cudaIpcMemLazyEnablePeerAccess));
         h->ipc_open.push_back(base);
@@ -1301,6 +1342,8 @@ int lbm_cuboid_p2p_connect(lbm_cuboid_t* h, const void* blob_down, const void* b
   }
   // flag words: [0] is written by the slab below, [1] by the slab above
   h->peer_flag_dn = peers[0] >= 0 ? (unsigned int*)m[0][2] + 1 : nullptr;
+  h->peer_rho_dn = (double*)m[0][3];
+  h->peer_rho_up = (double*)m[1][3];
   h->peer_flag_up = peers[1] >= 0 ? (unsigned int*)m[1][2] + 0 : nullptr;
   h->p2p_ready = true;
   return LBM_OK;

@@ -34,7 +34,7 @@ for w in cases:
                        {"streaming": 1, "graphs": 2}, {"halo": 2}, {"graphs": 3}, {"fd_two_pass": 1}):
                 if kw.get("halo") and ww.bc[4] != 0:
                     continue
-                if ("streaming" in kw or kw.get("halo") == 2) and ww.corrections == synth.CORR_FULL_FD:
+                if "streaming" in kw and ww.corrections == synth.CORR_FULL_FD:
                     continue
                 if "fd_two_pass" in kw:
                     if ww.corrections != synth.CORR_FULL_FD:

@@ -67,7 +67,7 @@ def _draw(rng):
     if roll < 0.25 and not fd:
         gpu["streaming"] = 1  # LBM_STREAM_AA: in-place streaming
         gpu["graphs"] = int(rng.choice([0, 1, 2]))
-    elif roll < 0.5 and not fd and bc[4] == PER:
+    elif roll < 0.5 and bc[4] == PER:
         gpu["halo"] = 2  # fused P2P halo, this slab its own neighbour
     return kw, gpu
 
