@@ -608,9 +608,12 @@ def test_full_fd_fused_kernel_bitwise_equal_two_pass(P, case, monkeypatch):
     a = _gpu(P, w, graphs=1, **kw)
     monkeypatch.setenv("LBM_FD_FUSED", "1")
     b = _gpu(P, w, graphs=1, **kw)
-    hs = [a, b]
+    monkeypatch.delenv("LBM_FD_FUSED")
+    hs = [a, b, _gpu(P, w, graphs=1, **kw)]  # and the default for this precision
     if w.bc[4] == synth.BC_PERIODIC:
+        monkeypatch.setenv("LBM_FD_FUSED", "1")
         hs.append(_gpu(P, w, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id(), **kw))
+        monkeypatch.delenv("LBM_FD_FUSED")
     for g in hs:
         g.init_fields(rho, u)
         g.step(23)
