@@ -1,7 +1,7 @@
 """Randomised parity: seeded random problem statements (grid, aspect ratios,
 cs2, all four relaxation rates, body force, every boundary kind on every axis,
 correction mode, collision model, storage precision, launch mode, streaming
-pattern, halo mode) through the C ABI against the CPU oracle, element by
+pattern, halo mode: in-kernel wrap, NCCL send-to-self, self-P2P) through the C ABI against the CPU oracle, element by
 element, after a few steps from non-equilibrium populations.
 
 Bars as in test_gpu_parity.py: fp64 max|df| <= 1e-12; fp32 storage
@@ -14,7 +14,7 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-N_CASES = 120
+N_CASES = 200
 PER, BB, MW, FS = 0, 1, 2, 3
 
 
@@ -67,8 +67,10 @@ def _draw(rng):
     if roll < 0.25 and not fd:
         gpu["streaming"] = 1  # LBM_STREAM_AA: in-place streaming
         gpu["graphs"] = int(rng.choice([0, 1, 2]))
-    elif roll < 0.5 and bc[4] == PER:
+    elif roll < 0.45 and bc[4] == PER:
         gpu["halo"] = 2  # fused P2P halo, this slab its own neighbour
+    elif roll < 0.6 and bc[4] == PER:
+        gpu["halo"] = 1  # NCCL ghost planes, sent to this rank itself
     return kw, gpu
 
 
@@ -85,6 +87,8 @@ def test_random_problem_matches_oracle(P, i):
     import oracle as O
 
     kw, gpu = CASES[i]
+    if gpu.get("halo") == 1:
+        gpu = dict(gpu, nccl_uid=P.nccl_unique_id())
     try:
         g = P.Lattice(**kw, **gpu)
     except P.LbmError as e:  # a drawn combination the ABI rejects must be a documented one
