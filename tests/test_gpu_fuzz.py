@@ -113,3 +113,66 @@ def test_random_problem_matches_oracle(P, i):
     else:
         err = (np.abs(fg - fo) / np.abs(fo)).max()
         assert err <= 1e-5, (err, kw, gpu)
+
+
+N_SLAB_CASES = 40
+
+
+def _slab_cases():
+    rng = np.random.Generator(np.random.PCG64(7413))
+    out = []
+    while len(out) < N_SLAB_CASES:
+        kw, _ = _draw(rng)
+        if kw["corrections"] == synth.CORR_FULL_FD:
+            continue  # FULL_FD exchanges within a step: slabs on one GPU cannot be stepped one at a time
+        world = int(rng.choice([2, 3, 4]))
+        kw["nz"] = world * int(rng.integers(1, 4))
+        out.append((kw, world))
+    return out
+
+
+SLAB_CASES = _slab_cases()
+
+
+@pytest.mark.parametrize("i", range(N_SLAB_CASES))
+def test_random_problem_p2p_slabs_match_oracle(P, i):
+    """Random problem statements split into 2-4 z-slabs wired with the fused P2P
+    halo (one process, direct pointers; slabs stepped one at a time), gathered
+    and compared with the oracle."""
+    import oracle as O
+
+    kw, world = SLAB_CASES[i]
+    try:
+        hs = [P.Lattice(**kw, rank=r, world=world, halo=2) for r in range(world)]
+    except P.LbmError as e:
+        assert e.code in (P.lbm.LBM_EINVAL, P.lbm.LBM_ENOTSUP), e
+        pytest.skip(f"rejected by the ABI: {e}")
+    blobs = [h.p2p_export() for h in hs]
+    for h in hs:
+        h.p2p_connect(*P.lbm.p2p_neighbour_blobs(P.lbm.halo_plan(h.p), blobs))
+    o = O.Oracle(**kw)
+    nx, ny, nz = kw["nx"], kw["ny"], kw["nz"]
+    rho, u = synth.random_fields(nx, ny, nz, 700 + i)
+    o.init_fields(rho, u)
+    f0 = o.get_populations() * (1.0 + 1e-3 * synth.noise((27, nz, ny, nx), 1700 + i))
+    o.set_populations(f0)
+    n = nz // world
+    for r, h in enumerate(hs):
+        h.set_populations(np.ascontiguousarray(f0[:, r * n:(r + 1) * n]))
+        h.sync()
+    steps = 9
+    for _ in range(steps):
+        for h in hs:
+            h.step(1)
+            h.sync()
+    o.step(steps)
+    fg = np.concatenate([h.get_populations() for h in hs], axis=1)
+    for h in hs:
+        h.close()
+    fo = o.get_populations()
+    if kw["precision"] == 0:
+        err = np.abs(fg - fo).max()
+        assert err <= 1e-12, (err, kw, world)
+    else:
+        err = (np.abs(fg - fo) / np.abs(fo)).max()
+        assert err <= 1e-5, (err, kw, world)
