@@ -85,7 +85,7 @@ struct lbm_cuboid {
   bool own_stream = false;
   cudaEvent_t ev_bnd = nullptr, ev_halo = nullptr;
   bool halo_pending = false;
-  bool ghost = false;  // ghost-plane (NCCL) mode
+  bool ghost = false;  // ghost-plane mode (NCCL or fused P2P halo)
   bool paper_rates = false;  // omega_1 = omega_high = 1 -> k_collide_stream_paper
   bool fd = false;           // FULL_FD: density pass + isotropic gradient
   bool fd_fused = true;      // FULL_FD: fused 2.5D kernel (fp64) or density pass + collide (fp32);
