@@ -158,6 +158,19 @@ def ncu_traffic(workload_name, precision):
 
 
 # --------------------------------------------------------------- cpu oracle
+def host_cpu():
+    """(CPU model, logical cores) of this host, for the cpu_baseline record."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
 def oracle_mlups(w, budget_s=15.0, grid=(64, 64, 32), max_steps=None):
     """The CPU oracle as it stands (single thread), on a bounded sample of the
     workload: same physics on a smaller grid, as many steps as fit in budget_s."""
@@ -204,7 +217,8 @@ def run_reference(args):
             "ms_per_step": el / steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": w.name, "nodes_global": w.nodes, "sample": sample},
-            "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle", "sample": sample,
+                             "cpu_model": host_cpu()[0], "host_logical_cores": host_cpu()[1]},
             "e2e": {"value": v, "unit": "MLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -374,7 +388,8 @@ def run_cuda(args):
     if world == 1 and not args.no_cpu_baseline:
         v, n, ws = oracle_mlups(w, budget_s=12.0)
         cpu = {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle",
-               "sample": f"{n} steps of {ws.nx}x{ws.ny}x{ws.nz} (same physics as {w.name}), single thread"}
+               "sample": f"{n} steps of {ws.nx}x{ws.ny}x{ws.nz} (same physics as {w.name}), single thread",
+               "cpu_model": host_cpu()[0], "host_logical_cores": host_cpu()[1]}
     line = {"metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
             "scaling": "weak" if args.workload == "weak" else "strong", "vs_baseline": None,
