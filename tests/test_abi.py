@@ -128,3 +128,15 @@ def test_params_struct_layout_matches_header(P, tmp_path):
     body = hdr[hdr.index("typedef struct {"):hdr.index("} lbm_cuboid_params;")]
     names = re.findall(r"[\s*](\w+)\s*(?:\[\d+\])?\s*[,;]", body)
     assert sorted(names) == sorted(fields), (sorted(names), sorted(fields))
+
+
+def test_plane_size_limit(P):
+    """27 nx ny must stay below 2^31 (int32 offsets within a plane): the largest
+    accepted plane and the first rejected one."""
+    lim = (2 ** 31 - 1) // 27
+    nx = 8191
+    ok_ny = lim // nx
+    assert P.lbm.buffer_bytes(P.lbm.make_params(nx, ok_ny, 2, 1.0, 2.0, omega_nu=1.5)) > 0
+    with pytest.raises(P.LbmError) as ei:
+        P.lbm.buffer_bytes(P.lbm.make_params(nx, ok_ny + 1, 2, 1.0, 2.0, omega_nu=1.5))
+    assert ei.value.code == P.lbm.LBM_EINVAL

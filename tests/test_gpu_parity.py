@@ -622,3 +622,40 @@ def test_full_fd_fused_kernel_bitwise_equal_two_pass(P, case, monkeypatch):
         assert np.array_equal(fa, g.get_populations())
     for g in hs:
         g.close()
+
+
+def test_max_plane_size_int32_offsets(P):
+    """The largest plane the ABI accepts (27 nx ny < 2^31: int32 offsets within a
+    plane): 8191 x 9710 nodes per plane, nz = 2 periodic, fp32 storage (69 GB in
+    two buffers).  One step from rough random fields; sampled nodes including all
+    four plane corners and the last node against the oracle's patch update.  The
+    populations are read straight from the device buffer (layout of DESIGN.md
+    section 6: [(z_local + 1) * 27 + q][y][x], q = (ex+1) + 3(ey+1) + 9(ez+1))."""
+    import oracle as O
+    import torch
+
+    nx, ny, nz = 8191, 9710, 2
+    assert 27 * nx * ny < 2 ** 31
+    w = synth.CONFIGS["tgv"].scaled(nx=nx, ny=ny, nz=nz, precision=synth.PREC_FP32)
+    free, _ = torch.cuda.mem_get_info()
+    if free < 80e9:
+        pytest.skip("needs ~75 GB of free device memory")
+    rho, u = synth.random_fields(nx, ny, nz, 4242)
+    g = _gpu(P, w)
+    g.init_fields(rho, u)
+    g.step(1)
+    g.sync()
+    buf = g._bufs[g.info()["steps"] % 2].view(torch.float32)  # the state after one step
+    e = O.velocities(1.0, 1.0).round().astype(int)           # paper order, unit components
+    qint = (e[:, 0] + 1) + 3 * (e[:, 1] + 1) + 9 * (e[:, 2] + 1)
+    nxy = nx * ny
+    rng = np.random.default_rng(5)
+    pts = [(0, 0), (nx - 1, 0), (0, ny - 1), (nx - 1, ny - 1), (nx // 2, ny // 2)]
+    pts += [(int(a), int(b)) for a, b in zip(rng.integers(0, nx, 4), rng.integers(0, ny, 4))]
+    for z in (0, nz - 1):
+        for x, y in pts:
+            off = torch.tensor([((z + 1) * 27 + int(q)) * nxy + y * nx + x for q in qint], device=buf.device)
+            fg = buf[off].double().cpu().numpy()
+            ref = _patch_update(w, rho, u, x, y, z)
+            assert (np.abs(fg - ref) / np.abs(ref)).max() <= TOL32, (x, y, z)
+    g.close()
