@@ -12,12 +12,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "build", "fd_variants")
 VARIANTS = {
-    "sync_zc32_ty4": ["LBM_FD_ASYNC=0", "LBM_FD_ZC=32", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
-    "async_zc32_ty4": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=32", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
-    "async_zc32_ty4_m3": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=32", "LBM_FD_TY=4", "LBM_FD_MINB=3"],
-    "async_zc32_ty2": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=32", "LBM_FD_TY=2", "LBM_FD_MINB=6"],
-    "async_zc32_ty8": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=32", "LBM_FD_TY=8", "LBM_FD_MINB=1"],
-    "async_zc64_ty4": ["LBM_FD_ASYNC=1", "LBM_FD_ZC=64", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
+    "fused": ["LBM_FD_RING_NOINLINE=0"],
+    "fused_ring_noinline": ["LBM_FD_RING_NOINLINE=1"],
 }
 
 if sys.argv[1] == "build":
@@ -29,10 +25,10 @@ if sys.argv[1] == "build":
         B.build(out=out, defines=d)
         log = open(out + ".ptxas.log").read()
         m = re.search(r"k_collide_stream_fdIdLi1EE.*?\n.*?(\d+) bytes spill stores.*?\n.*?Used (\d+) registers", log, re.S)
-        print(n, "spill", m.group(1), "regs", m.group(2))
+        print(n, "spill", m.group(1) if m else "?", "regs", m.group(2) if m else "?")
 else:
     for n in VARIANTS:
-        env = dict(os.environ, LBM_CUBOID_LIB=os.path.join(VDIR, f"lib_{n}.so"))
+        env = dict(os.environ, LBM_CUBOID_LIB=os.path.join(VDIR, f"lib_{n}.so"), LBM_FD_FUSED="1")
         r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "10", "--warmup", "3",
                             "--corrections", "full_fd", "--no-e2e", "--no-cpu-baseline"],
                            capture_output=True, text=True, env=env, timeout=300)
