@@ -11,9 +11,12 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "build", "fd_variants")
-VARIANTS = {
-    "fused": ["LBM_FD_RING_NOINLINE=0"],
-    "fused_ring_noinline": ["LBM_FD_RING_NOINLINE=1"],
+VARIANTS = {  # tile / chunk shapes of the fused FULL_FD kernel
+    "zc32_ty4": ["LBM_FD_ZC=32", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
+    "zc16_ty4": ["LBM_FD_ZC=16", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
+    "zc64_ty4": ["LBM_FD_ZC=64", "LBM_FD_TY=4", "LBM_FD_MINB=4"],
+    "zc32_ty8": ["LBM_FD_ZC=32", "LBM_FD_TY=8", "LBM_FD_MINB=2"],
+    "zc32_tx64_ty4": ["LBM_FD_ZC=32", "LBM_FD_TX=64", "LBM_FD_TY=4", "LBM_FD_MINB=2"],
 }
 
 if sys.argv[1] == "build":
