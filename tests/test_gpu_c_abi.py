@@ -39,3 +39,30 @@ def test_c_program_matches_python_binding(tmp_path):
     assert np.abs(data[:n].reshape(rp.shape) - rp).max() < 1e-13
     assert np.abs(data[n:].reshape(up.shape) - up).max() < 1e-13
     assert '"mass_change"' in r.stdout
+
+
+@pytest.mark.parametrize("halo", ["nccl", "p2p"])
+def test_multi_gpu_example_runs_on_one_gpu(halo):
+    """examples/multi_gpu_tgv.py under torchrun with one process: runs, and the
+    kinetic energy decays within 0.1 % of the linear Taylor-Green rate."""
+    import re
+    import socket
+    import sys
+
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port),
+                        os.path.join(ROOT, "examples", "multi_gpu_tgv.py"), "--halo", halo, "--n", "128",
+                        "--steps", "200"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    m = re.search(r"KE ratio ([0-9.]+) \(linear theory ([0-9.]+)\)", r.stdout)
+    assert m, r.stdout
+    assert abs(float(m.group(1)) / float(m.group(2)) - 1.0) < 1e-3
