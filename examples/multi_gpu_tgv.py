@@ -1,7 +1,7 @@
 """Multi-GPU Taylor-Green vortex through the Python binding (one process per GPU).
 
   python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
-      examples/multi_gpu_tgv.py [--halo nccl|p2p] [--n 256] [--steps 500]
+      examples/multi_gpu_tgv.py [--halo nccl|p2p] [--grid 256] [--steps 500]
 
 Each rank owns a z-slab of an n x n x n/2 lattice (r = 1, s = 2: a cubic
 physical box), initialises its slab of the decaying Taylor-Green vortex,
@@ -26,7 +26,7 @@ import synth  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--halo", choices=["nccl", "p2p"], default="nccl")
-    ap.add_argument("--n", type=int, default=256)
+    ap.add_argument("--grid", type=int, default=256, help="nodes along x and y (nz = grid/2)")
     ap.add_argument("--steps", type=int, default=500)
     args = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -34,7 +34,7 @@ def main():
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     world, rank = dist.get_world_size(), dist.get_rank()
 
-    w = synth.CONFIGS["weak"].scaled(nx=args.n, ny=args.n, nz=args.n // 2, u0=1e-3)
+    w = synth.CONFIGS["weak"].scaled(nx=args.grid, ny=args.grid, nz=args.grid // 2, u0=1e-3)
     halo = P.HALO_P2P if args.halo == "p2p" else P.HALO_AUTO
     lat = P.distributed_lattice(device=local, halo=halo, **w.params())
     z0, z1 = synth.slab_range(w.nz, rank, world)
