@@ -65,8 +65,16 @@ struct Consts {
   double lid_c[3];            // Eq. 69 coefficient per e_z in {-1,0,1}: cs2/(2 r^2) * phi_z(e_z)
   double phx[3], phy[3], phz[3];  // cuboid rest weights per axis: phi(0) = 1 - cs2/c^2, phi(+-1) = cs2/(2c^2)
   long long buf_elems;        // elements of one population buffer (bounds checks)
+  unsigned int nx_mul;        // fast division by nx (row of a plane index): see row_of()
+  int nx_shift;
   unsigned int* dbg_flag;     // LBM_DEBUG_BOUNDS builds: set to 1 on an out-of-range access
 };
+
+// Row y = idx / nx of a plane index idx < 2^31 by multiply-high and shift
+// (round-up reciprocal, exact for 31-bit dividends; host side: fill_consts).
+__device__ __forceinline__ int row_of(const Consts& c, int idx) {
+  return c.nx_mul ? int(__umulhi((unsigned)idx, c.nx_mul) >> c.nx_shift) : idx;
+}
 
 // Debug builds (-DLBM_DEBUG_BOUNDS): every population access of the collide-stream
 // kernels is checked against the buffer; a violation sets *dbg_flag and is skipped.
@@ -324,7 +332,28 @@ __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int
   // warp-uniform choice: a warp with any wall-adjacent lane takes the wall path
   // (which reduces to the plain pull for its other lanes) instead of running
   // both paths one after the other
-  const bool wall = __any_sync(__activemask(), ps.wall);
+  const unsigned mask = __activemask();
+  const bool wall = __any_sync(mask, ps.wall);
+  // no lane of the warp wraps around a periodic face: every source is the own
+  // node's address plus an offset that is the same for the whole warp
+  // ((-e_z) plane + slot nxy - e_y nx - e_x), so the 27 addresses need no
+  // per-lane index arithmetic (ghost planes included)
+  const bool lane_inner = (x > 0 && x < nx - 1 && y > 0 && y < c.ny - 1 &&
+                           !(z == 0 && c.face[4] == FK_WRAP) && !(z == c.nzl - 1 && c.face[5] == FK_WRAP));
+  if (!wall && __all_sync(mask, lane_inner)) {
+    const T* b = src + (long long)(z + 1) * c.plane + (y * nx + x);
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int q = LBM_Q(i, j, k);
+          const long long off = (long long)(1 - k) * c.plane + (long long)(slot(q) * c.nxy + (1 - j) * nx + (1 - i));
+          f[q] = ldg(LBM_CHECK_LD(src, b + off, c));
+        }
+    return;
+  }
   if (!wall) {
 #pragma unroll
     for (int k = 0; k < 3; ++k)
@@ -459,7 +488,7 @@ __global__ void __launch_bounds__(kBlock) k_density(const T* __restrict__ src, d
                                                     const __grid_constant__ Consts c, int zbeg, int zstride) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
-  const int y = idx / c.nx;
+  const int y = row_of(c, idx);
   const int x = idx - y * c.nx;
   const int z = zbeg + blockIdx.y * zstride;
   double f[27];
@@ -944,7 +973,7 @@ __device__ __forceinline__ void collide_stream_ab(const T* __restrict__ src, T* 
                                                   int zstride) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
-  const int y = idx / c.nx;
+  const int y = row_of(c, idx);
   const int x = idx - y * c.nx;
   const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
   double f[27];
@@ -1088,7 +1117,7 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_p2p(const T* __restrict__ src, T*
                                                    int zbeg, int zstride, const P2PArgs<T> a) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx < c.nxy) {  // no early return: every thread reaches the barrier of p2p_signal
-    const int y = idx / c.nx;
+    const int y = row_of(c, idx);
     const int x = idx - y * c.nx;
     const int z = zbeg + blockIdx.y * zstride;
     double gxr = 0.0, gyr = 0.0, gzr = 0.0;
@@ -1123,7 +1152,7 @@ __global__ void __launch_bounds__(kBlock) k_density_p2p(const T* __restrict__ sr
                                                         const P2PArgs<double> a) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx < c.nxy) {
-    const int y = idx / c.nx;
+    const int y = row_of(c, idx);
     const int z = pl.z[blockIdx.y];
     double f[27];
     gather<T>(src, c, idx - y * c.nx, y, z, f);
@@ -1177,7 +1206,7 @@ __global__ void LBM_CS_BOUNDS k_persistent(T* __restrict__ b0, T* __restrict__ b
       for (long long n = first; n < nodes; n += stride) {
         const int z = int(n / c.nxy);
         const int idx = int(n - (long long)z * c.nxy);
-        const int y = idx / c.nx;
+        const int y = row_of(c, idx);
         double f[27];
         gather<T>(src, c, idx - y * c.nx, y, z, f);
         double r0 = 0.0;
@@ -1190,7 +1219,7 @@ __global__ void LBM_CS_BOUNDS k_persistent(T* __restrict__ b0, T* __restrict__ b
     for (long long n = first; n < nodes; n += stride) {
       const int z = int(n / c.nxy);
       const int idx = int(n - (long long)z * c.nxy);
-      const int y = idx / c.nx;
+      const int y = row_of(c, idx);
       const int x = idx - y * c.nx;
       double gxr = 0.0, gyr = 0.0, gzr = 0.0;
       if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
@@ -1216,7 +1245,7 @@ template <typename T, int KIND, bool ODD>
 __global__ void LBM_CS_BOUNDS k_aa(T* buf, const __grid_constant__ Consts c, int zbeg, int zstride) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
-  const int y = idx / c.nx;
+  const int y = row_of(c, idx);
   const int x = idx - y * c.nx;
   const int z = zbeg + blockIdx.y * zstride;
   double f[27];
@@ -1327,7 +1356,7 @@ __device__ __forceinline__ void load_canonical(const T* src, const Consts& c, in
 #pragma unroll
     for (int q = 0; q < 27; ++q) f[q] = ldg(p + q * c.nxy);
   } else {
-    const int y = idx / c.nx;
+    const int y = row_of(c, idx);
     aa_canonical<T>(src, c, idx - y * c.nx, y, z, aa == 1 ? 1 : 2, f);
   }
 }

@@ -246,6 +246,18 @@ void fill_consts(lbm_cuboid* h) {
     c.face[5] = kind(p.bc[5]);
   }
   c.buf_elems = h->buf_elems;
+  // fast division by nx for idx < 2^31: m = ceil(2^p / nx), p = 31 + ceil(log2 nx),
+  // idx / nx = umulhi(idx, m) >> (p - 32)  (nx = 1: no division)
+  if (p.nx > 1) {
+    int l = 0;
+    while ((1u << l) < unsigned(p.nx)) ++l;
+    const int pw = 31 + l;
+    c.nx_mul = unsigned(((uint64_t(1) << pw) + uint64_t(p.nx) - 1) / uint64_t(p.nx));
+    c.nx_shift = pw - 32;
+  } else {
+    c.nx_mul = 0;
+    c.nx_shift = 0;
+  }
   // rest weights of the isotropic density gradient (FULL_FD): f^eq at rho = 1, u = 0 per axis
   const double cc[3] = {1.0, c.r2, c.s2};
   double* ph[3] = {c.phx, c.phy, c.phz};
