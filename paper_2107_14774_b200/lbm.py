@@ -190,9 +190,15 @@ class Lattice:
         self.device = torch.device("cuda", int(device))
         nbytes = buffer_bytes(self.p)
         nbuf = 1 if int(streaming) == STREAM_AA else 2
-        self._bufs = [torch.empty(nbytes, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
-        self.p.buf_a = self._bufs[0].data_ptr()
-        self.p.buf_b = self._bufs[1].data_ptr() if nbuf == 2 else None
+        if int(halo) == HALO_P2P and int(world) > 1:
+            # buffers shared with other processes through CUDA IPC: plain cudaMalloc
+            # allocations owned by the library (torch's allocator may hand out
+            # memory that cannot be exported, e.g. expandable segments)
+            self._bufs = []
+        else:
+            self._bufs = [torch.empty(nbytes, dtype=torch.uint8, device=self.device) for _ in range(nbuf)]
+            self.p.buf_a = self._bufs[0].data_ptr()
+            self.p.buf_b = self._bufs[1].data_ptr() if nbuf == 2 else None
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
             if stream.cuda_stream == 0:
