@@ -106,6 +106,7 @@ struct lbm_cuboid {
   unsigned int* peer_flag_dn = nullptr;  // my slot in the down neighbour's flag words ([1])
   std::vector<void*> ipc_open;           // IPC mappings to close
   uint32_t epoch = 0;                    // halo publishes enqueued so far
+  void* wait32 = nullptr;                // cuStreamWaitValue32 (driver entry point, resolved at create)
   cudaEvent_t ev_fork = nullptr;
   Consts c{};
   double* stage = nullptr;
@@ -680,9 +681,7 @@ int p2p_join(lbm_cuboid* h) {
 // (their last reader was their publish e or earlier).  Stream-ordered wait on
 // the flag words in this GPU's memory; nothing spins.
 int p2p_wait(lbm_cuboid* h) {
-  static PfnWaitValue32 wait32 = nullptr;
-  int rc;
-  if (!wait32 && (rc = driver_fn("cuStreamWaitValue32", &wait32))) return rc;
+  const PfnWaitValue32 wait32 = reinterpret_cast<PfnWaitValue32>(h->wait32);
   const CUstream cs = (CUstream)h->comm_stream;
   if (h->peer_down >= 0) {
     CUresult r = wait32(cs, (CUdeviceptr)(h->d_sig + 0), h->epoch, CU_STREAM_WAIT_VALUE_GEQ);
@@ -986,6 +985,9 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
         cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess)
       return bail(fail(LBM_ECUDA, "stream/event creation failed"));
+    PfnWaitValue32 w32 = nullptr;
+    if ((rc = driver_fn("cuStreamWaitValue32", &w32))) return bail(rc);
+    h->wait32 = reinterpret_cast<void*>(w32);
     if (cudaMalloc(&h->d_sig, 4 * sizeof(unsigned int)) != cudaSuccess ||
         cudaMemsetAsync(h->d_sig, 0, 4 * sizeof(unsigned int), h->stream) != cudaSuccess)
       return bail(fail(LBM_ENOMEM, "cudaMalloc of the P2P flag words failed"));
