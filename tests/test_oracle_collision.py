@@ -79,6 +79,27 @@ def test_corrections_vanish_on_cubic_lattice():
         assert 0 < d < 1e-3
 
 
+def test_correction_order_cubic_vs_cuboid():
+    """on the cubic lattice (r = s = 1, cs2 = 1/3) FULL_LOCAL differs
+    from the uncorrected scheme only by the Galilean-invariance term
+    -3 rho u^2 (1/omega - 1/2) times the strain, O(u^2 * noneq): with u and the
+    non-equilibrium both scaled by a, the difference scales as a^3 (slope 3).
+    On the cuboid lattice (s = 2) the (3 cs2 - s^2) term is O(1): slope 1."""
+    rng = np.random.default_rng(11)
+    u0, d = rng.uniform(-1, 1, 3), rng.uniform(-1, 1, 27)
+    kw = dict(omega_nu=1.6, omega_xi=1.2)
+
+    def diff(r, s, a):
+        f = U.feq_product(r, s, 1 / 3, 1.0, a * u0) * (1.0 + a * d)
+        full = O.Oracle(2, 2, 2, r, s, 1 / 3, corrections=FULL, **kw).collide(f)
+        off = O.Oracle(2, 2, 2, r, s, 1 / 3, corrections=OFF, **kw).collide(f)
+        return np.abs(full - off).max()
+
+    for a in (0.02, 0.01):
+        assert np.log2(diff(1.0, 1.0, a) / diff(1.0, 1.0, a / 2)) == pytest.approx(3.0, abs=0.05)
+        assert np.log2(diff(1.0, 2.0, a) / diff(1.0, 2.0, a / 2)) == pytest.approx(1.0, abs=0.05)
+
+
 def test_corrections_active_on_cuboid_lattice():
     """At s = 2 the (3 cs2 - s^2) term is O(1): FULL/LOW differ from OFF at
     first order in the non-equilibrium, and not at equilibrium."""
