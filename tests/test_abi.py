@@ -140,3 +140,27 @@ def test_plane_size_limit(P):
     with pytest.raises(P.LbmError) as ei:
         P.lbm.buffer_bytes(P.lbm.make_params(nx, ok_ny + 1, 2, 1.0, 2.0, omega_nu=1.5))
     assert ei.value.code == P.lbm.LBM_EINVAL
+
+
+def test_mode_validation(P):
+    """Launch/halo/streaming mode fields: out-of-range values are LBM_EINVAL,
+    unsupported combinations LBM_ENOTSUP (host-side, no GPU)."""
+    mk, bb = P.lbm.make_params, P.lbm.buffer_bytes
+    base = dict(nx=8, ny=4, nz=6, r=1.0, s=2.0, omega_nu=1.5)
+    for kw, code in [(dict(halo=3), P.lbm.LBM_EINVAL), (dict(graphs=4), P.lbm.LBM_EINVAL),
+                     (dict(graphs=-1), P.lbm.LBM_EINVAL), (dict(streaming=2), P.lbm.LBM_EINVAL),
+                     (dict(model=2), P.lbm.LBM_EINVAL), (dict(precision=2), P.lbm.LBM_EINVAL),
+                     (dict(streaming=1, halo=2), P.lbm.LBM_ENOTSUP),
+                     (dict(streaming=1, halo=1), P.lbm.LBM_ENOTSUP),
+                     (dict(streaming=1, world=2, rank=0), P.lbm.LBM_ENOTSUP),
+                     (dict(streaming=1, corrections=3), P.lbm.LBM_ENOTSUP)]:
+        d = dict(base)
+        d.update(kw)
+        with pytest.raises(P.LbmError) as ei:
+            bb(mk(**d))
+        assert ei.value.code == code, (kw, ei.value)
+    # accepted: P2P with FULL_FD, the persistent launch mode, fp32 storage
+    for kw in (dict(halo=2, corrections=3), dict(graphs=3), dict(precision=1, graphs=3)):
+        d = dict(base)
+        d.update(kw)
+        assert bb(mk(**d)) > 0
