@@ -110,7 +110,8 @@ def config3(steps=20000):
         w = synth.CONFIGS[key]
         res = {"config": w.name, "steps": steps}
         prof = {}
-        for label, ww in (("cuboid", w), ("cubic", w.scaled(nz=256, s=1.0))):
+        for label, ww in (("cuboid", w), ("cuboid_fp32_storage", w.scaled(precision=synth.PREC_FP32)),
+                          ("cubic", w.scaled(nz=256, s=1.0))):
             lat = _lat(ww)
             rho, u = synth.rest_fields(ww.nx, ww.ny, ww.nz)
             lat.init_fields(rho, u)
@@ -125,6 +126,9 @@ def config3(steps=20000):
             lat.close()
         res["max_abs_du_over_U"] = float(np.abs(prof["cuboid"][0] - prof["cubic"][0]).max())
         res["max_abs_dv_over_U"] = float(np.abs(prof["cuboid"][1] - prof["cubic"][1]).max())
+        # BASELINE config 3 asks for the fp32-storage variant too: same grid, fp32 populations
+        res["fp32_vs_fp64_max_abs_du_over_U"] = float(np.abs(prof["cuboid_fp32_storage"][0] - prof["cuboid"][0]).max())
+        res["fp32_vs_fp64_max_abs_dv_over_U"] = float(np.abs(prof["cuboid_fp32_storage"][1] - prof["cuboid"][1]).max())
         res["u_min_over_U_cuboid"] = float(prof["cuboid"][0].min())
         res["u_min_over_U_cubic"] = float(prof["cubic"][0].min())
         out.append(res)
