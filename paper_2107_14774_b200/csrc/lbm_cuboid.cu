@@ -19,6 +19,7 @@
 #include "cm_kernels.cuh"
 
 #include <cuda.h>  // driver types only; entry points come from cudaGetDriverEntryPointByVersion
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys (no-ops without a tool)
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <unistd.h>
@@ -39,6 +40,12 @@ using lbm::Consts;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range for the scope of a host call (step phases show up in nsys timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -585,6 +592,7 @@ int p2p_push(lbm_cuboid* h, int which);
 // planes, on the comm stream, after the work already enqueued on the compute stream.
 int exchange(lbm_cuboid* h, int which) {
   if (!h->ghost) return LBM_OK;
+  NvtxRange nv("lbm halo exchange");
   if (h->p2p) return p2p_push(h, which);
   CU(cudaEventRecord(h->ev_bnd, h->stream));
   CU(cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
@@ -720,6 +728,7 @@ int p2p_push(lbm_cuboid* h, int which) {
 // (storing into the neighbours' ghost planes of buffer cur ^ 1), interior
 // planes concurrently on the compute stream, then join.
 int p2p_step(lbm_cuboid* h) {
+  NvtxRange nv("lbm step (P2P halo)");
   int rc;
   if ((rc = p2p_ready(h))) return rc;
   const int which = h->cur ^ 1;
@@ -832,6 +841,7 @@ int step_once(lbm_cuboid* h) {
   void* dst = h->buf[h->cur ^ 1];
   if (h->aa) return launch_aa(h, h->stream);
   if (h->p2p) return p2p_step(h);
+  NvtxRange nv(h->ghost ? "lbm step (NCCL halo)" : "lbm step");
   if (!h->ghost) {
     if (h->fd && !h->fd_fused && (rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
     return launch_cs(h, src, dst, 0, h->nzl, 1, h->stream);
@@ -1053,6 +1063,7 @@ int lbm_cuboid_init_fields(lbm_cuboid_t* h, const double* rho, const double* u) 
 
 int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
+  NvtxRange nv("lbm_cuboid_step");
   if (nsteps < 0) return fail(LBM_EINVAL, "nsteps must be >= 0");
   int rc = set_device(h);
   if (rc) return rc;
