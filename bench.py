@@ -396,7 +396,7 @@ def run_cuda(args):
             "dtype": "f64" if prec == "fp64" else "f64-arith/f32-storage", "data": "synthetic",
             "config": {"workload": w.name, "grid_global": [w.nx, w.ny, w.nz], "nodes_global": w.nodes,
                        "r": w.r, "s": w.s, "nu": w.nu, "corrections": args.corrections.upper(),
-                       "model": "3DCCM" if w.model == 0 else "3DCRM", "storage": prec,
+                       "collision": "3DCCM" if w.model == 0 else "3DCRM", "storage": prec,
                        "l2": ("working set per step >> 126 MB L2; no flush needed" if flush is None else
                               f"buffers ({lat.info()['buffer_bytes'] / 1e6:.1f} MB each) fit in L2: 512 MB L2 "
                               "flush (untimed) before every step, per-step CUDA events summed"),
