@@ -94,11 +94,42 @@ def run_case(name, n=25, U=(0.0, 0.0, 0.0)):
             "max_abs_lambda": m, "at_kappa": [float(x) for x in k]}
 
 
+def max_stable_speed(r, s, cs2, omega_nu, model, omega_xi=1.0, n=15, du=0.025, u_max=0.6):
+    """Largest uniform speed U along x (steps of du) for which the linearised
+    update is stable on an n^3 grid (None if unstable at rest): the linear
+    counterpart of the paper's section-7 robustness study."""
+    o = O.Oracle(2, 2, 2, r, s, cs2, omega_nu, omega_xi=omega_xi, corrections=synth.CORR_FULL_LOCAL, model=model)
+    best = None
+    for U in np.arange(0.0, u_max + 1e-12, du):
+        m, _ = max_growth(collision_jacobian(o, r, s, (float(U), 0.0, 0.0)), n)
+        if m > 1.0 + 1e-9:
+            break
+        best = float(U)
+    return best
+
+
+def main_mean_flow(out):
+    rows = []
+    for model in (0, 1):
+        for wn in (1.0, 1.4, 1.6, 1.8, 1.9):
+            u = max_stable_speed(0.5, 1.0, 0.08, wn, model)
+            rows.append({"model": "3DCRM" if model else "3DCCM", "r": 0.5, "s": 1.0, "cs2": 0.08, "omega_nu": wn,
+                         "omega_xi": 1.0, "max_linearly_stable_U": u})
+            print(json.dumps(rows[-1]), flush=True)
+    with open(out, "w") as fh:
+        json.dump(rows, fh, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=25)
     ap.add_argument("--out", default=os.path.join(ROOT, "results", "linear_stability.json"))
+    ap.add_argument("--mean-flow", action="store_true",
+                    help="max linearly stable uniform speed, CM vs RM (section-7 setting)")
     args = ap.parse_args()
+    if args.mean_flow:
+        main_mean_flow(os.path.join(ROOT, "results", "linear_stability_mean_flow.json"))
+        return
     res = [run_case(c, args.n) for c in CASES]
     res += [run_case(c, args.n, U=(0.05, 0.0, 0.0)) for c in ("config3_cavity_re1000", "config4_shear_layer")]
     for r in res:
