@@ -165,8 +165,9 @@ int lbm_cuboid_buffer_bytes(const lbm_cuboid_params *p, int64_t *bytes);
 int lbm_cuboid_halo_plan(const lbm_cuboid_params *p, int64_t out[8]);
 
 /* LBM_HALO_P2P wiring.  export: write this handle's LBM_P2P_BLOB_BYTES-byte
- * descriptor (IPC handles and addresses of both population buffers and of the
- * flag words, pid, geometry) into blob.  connect: map the neighbours' buffers
+ * descriptor (IPC handles and addresses of both population buffers, of the
+ * flag words and, with LBM_CORR_FULL_FD, of the density field; pid; geometry)
+ * into blob.  connect: map the neighbours' buffers
  * (blob_down = the rank below, blob_up = the rank above, as given by
  * lbm_cuboid_halo_plan; NULL where there is no neighbour; the same blob twice
  * when both neighbours are one rank).  Every rank calls connect once, after
@@ -186,7 +187,9 @@ int lbm_cuboid_p2p_connect(lbm_cuboid_t *h, const void *blob_down, const void *b
 /* Write a fresh 128-byte ncclUniqueId into out (call on rank 0 only). */
 int lbm_cuboid_nccl_unique_id(void *out128);
 
-/* Validate p (errors: LBM_EINVAL with a message naming the field), bind the
+/* Validate p (errors: LBM_EINVAL with a message naming the field, also for a
+ * strain-rate system of the corrections that is singular at rest;
+ * LBM_ENOTSUP for unsupported mode combinations), bind the
  * device, allocate/bind buffers, upload the parameter block and, if needed,
  * create the NCCL communicator (collective over all ranks). */
 int lbm_cuboid_create(const lbm_cuboid_params *p, lbm_cuboid_t **out);
