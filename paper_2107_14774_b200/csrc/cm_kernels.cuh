@@ -570,13 +570,21 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
+// Deterministic two-kernel reduction: every CTA of a grid-stride pass writes its
+// seven partials; one CTA then reduces them in a fixed order (no atomics: the
+// sums do not depend on scheduling).
+constexpr int kCheckThreads = 256;
+constexpr int kCheckMaxBlocks = 2048;
+
 template <typename T>
-__global__ void __launch_bounds__(kBlock) k_check(const T* __restrict__ src, double* __restrict__ out,
-                                                  const __grid_constant__ Consts c, int aa) {
-  const int idx = blockIdx.x * kBlock + threadIdx.x;
-  const int z = blockIdx.y;
+__global__ void __launch_bounds__(kCheckThreads) k_check(const T* __restrict__ src, double* __restrict__ partial,
+                                                         const __grid_constant__ Consts c, int aa) {
+  const long long nodes = (long long)c.nzl * c.nxy;
   double v[7] = {0, 0, 0, 0, 0, 0, 0};
-  if (idx < c.nxy) {
+  for (long long n = (long long)blockIdx.x * kCheckThreads + threadIdx.x; n < nodes;
+       n += (long long)gridDim.x * kCheckThreads) {
+    const int z = int(n / c.nxy);
+    const int idx = int(n - (long long)z * c.nxy);
     double fq[27];
     load_canonical<T>(src, c, idx, z, aa, fq);
     double rho = 0.0, jx = 0.0, jy = 0.0, jz = 0.0;
@@ -592,17 +600,16 @@ __global__ void __launch_bounds__(kBlock) k_check(const T* __restrict__ src, dou
     const double ux = (jx - 0.5 * c.F[0]) / rho, uy = (c.r * jy - 0.5 * c.F[1]) / rho,
                  uz = (c.s * jz - 0.5 * c.F[2]) / rho;
     const double u2 = ux * ux + uy * uy + uz * uz;
-    v[0] = rho;
-    v[1] = rho * ux;
-    v[2] = rho * uy;
-    v[3] = rho * uz;
-    v[4] = 0.5 * rho * u2;
-    v[5] = sqrt(u2);
     const bool bad = !(rho > 0.0) || !(u2 <= 1.0) || !isfinite(rho) || !isfinite(u2);
-    v[6] = bad ? 1.0 : 0.0;
-    if (bad) v[5] = 0.0;
+    v[0] += rho;
+    v[1] += rho * ux;
+    v[2] += rho * uy;
+    v[3] += rho * uz;
+    v[4] += 0.5 * rho * u2;
+    v[5] = bad ? v[5] : fmax(v[5], sqrt(u2));
+    v[6] += bad ? 1.0 : 0.0;
   }
-  __shared__ double sm[7][kBlock / 32];
+  __shared__ double sm[7][kCheckThreads / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
 #pragma unroll
   for (int t = 0; t < 7; ++t) {
@@ -613,13 +620,33 @@ __global__ void __launch_bounds__(kBlock) k_check(const T* __restrict__ src, dou
   if (threadIdx.x < 7) {
     const int t = threadIdx.x;
     double r = sm[t][0];
-    for (int i = 1; i < kBlock / 32; ++i) r = (t == 5) ? fmax(r, sm[t][i]) : r + sm[t][i];
-    if (t == 5)
-      atomicMax(reinterpret_cast<unsigned long long*>(out + 5), (unsigned long long)__double_as_longlong(r));
-    else
-      atomicAdd(out + t, r);
+    for (int i = 1; i < kCheckThreads / 32; ++i) r = (t == 5) ? fmax(r, sm[t][i]) : r + sm[t][i];
+    partial[(long long)blockIdx.x * 8 + t] = r;
   }
 }
+
+__global__ void __launch_bounds__(kCheckThreads) k_check_final(const double* __restrict__ partial, int nblocks,
+                                                               double* __restrict__ out) {
+  double v[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int b = threadIdx.x; b < nblocks; b += kCheckThreads)
+#pragma unroll
+    for (int t = 0; t < 7; ++t) v[t] = (t == 5) ? fmax(v[t], partial[b * 8 + t]) : v[t] + partial[b * 8 + t];
+  __shared__ double sm[7][kCheckThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < 7; ++t) {
+    const double r = (t == 5) ? warp_max(v[t]) : warp_sum(v[t]);
+    if (lane == 0) sm[t][w] = r;
+  }
+  __syncthreads();
+  if (threadIdx.x < 7) {
+    const int t = threadIdx.x;
+    double r = sm[t][0];
+    for (int i = 1; i < kCheckThreads / 32; ++i) r = (t == 5) ? fmax(r, sm[t][i]) : r + sm[t][i];
+    out[t] = r;
+  }
+}
+
 
 
 }  // namespace lbm

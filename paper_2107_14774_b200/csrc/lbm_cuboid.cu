@@ -976,7 +976,9 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   for (int i = 0; i < nbuf; ++i)
     if (cudaMemsetAsync(h->buf[i], 0, bytes, h->stream) != cudaSuccess)
       return bail(fail(LBM_ECUDA, "cudaMemsetAsync failed"));
-  if (cudaMalloc(&h->d_check, 8 * sizeof(double)) != cudaSuccess) return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
+  // check(): 8 result slots + 8 partials per reduction block
+  if (cudaMalloc(&h->d_check, size_t(8) * (1 + lbm::kCheckMaxBlocks) * sizeof(double)) != cudaSuccess)
+    return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
   if (cudaMalloc(&h->d_dbg, sizeof(unsigned int)) != cudaSuccess ||
       cudaMemsetAsync(h->d_dbg, 0, sizeof(unsigned int), h->stream) != cudaSuccess)
     return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
@@ -1190,16 +1192,22 @@ int lbm_cuboid_check(lbm_cuboid_t* h, double out[7]) {
   if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
   int rc = set_device(h);
   if (rc) return rc;
-  CU(cudaMemsetAsync(h->d_check, 0, 8 * sizeof(double), h->stream));
-  dim3 g = grid_for(h, h->nzl);
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->p.device));
+  const int64_t nodes = h->nxy * h->nzl;
+  const int nb = int(std::max<int64_t>(1, std::min<int64_t>({(nodes + lbm::kCheckThreads - 1) / lbm::kCheckThreads,
+                                                            int64_t(8) * sms, int64_t(lbm::kCheckMaxBlocks)})));
+  double* partial = h->d_check + 8;
   if (h->p.precision == LBM_FP64)
-    lbm::k_check<double><<<g, lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], h->d_check, h->c,
-                                                           aa_mode(h));
+    lbm::k_check<double><<<nb, lbm::kCheckThreads, 0, h->stream>>>((const double*)h->buf[h->cur], partial, h->c,
+                                                                   aa_mode(h));
   else
-    lbm::k_check<float><<<g, lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], h->d_check, h->c,
-                                                          aa_mode(h));
+    lbm::k_check<float><<<nb, lbm::kCheckThreads, 0, h->stream>>>((const float*)h->buf[h->cur], partial, h->c,
+                                                                  aa_mode(h));
   CU(cudaGetLastError());
-  h->launches++;
+  lbm::k_check_final<<<1, lbm::kCheckThreads, 0, h->stream>>>(partial, nb, h->d_check);
+  CU(cudaGetLastError());
+  h->launches += 2;
   CU(cudaMemcpyAsync(out, h->d_check, 7 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
   if (out[6] > 0) return fail(LBM_EUNSTABLE, "%.0f nodes with NaN, rho <= 0 or |u| > 1 after %lld steps", out[6],
