@@ -35,9 +35,11 @@
  * isotropic lattice gradient of the same-time density).
  *
  * Parity pins: tests/test_oracle_*.py (closed forms, paper-printed appendices
- * and Eq. 69, conservation, SRT limit, analytic TGV/shear-wave/duct decay,
- * viscous and acoustic isotropy, Galilean invariance, moving-frame sound
- * attenuation for the density-gradient terms, Womersley).
+ * and Eq. 69, conservation, SRT limit, order of the corrections (slope 3 on the
+ * cubic lattice, 1 on the cuboid one), analytic TGV/shear-wave/duct decay,
+ * plane Couette flow under the moving lid, viscous and acoustic isotropy,
+ * Galilean invariance, moving-frame sound attenuation for the density-gradient
+ * terms, Womersley, long-wave eigenvalues of the linearised update).
  * The free-slip rule (reading R7) is not in the paper (BASELINE config 4 asks
  * for it); it is pinned by invariants (mass, tangential momentum) and by the
  * analytic decay nu k^2 of the cosine shear mode between stress-free walls
