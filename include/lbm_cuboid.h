@@ -196,14 +196,16 @@ int lbm_cuboid_create(const lbm_cuboid_params *p, lbm_cuboid_t **out);
 
 /* Initialise the stored state with f~ = f^eq(rho, u + F/(2 rho)) (DESIGN R8)
  * from HOST fields rho [nz_l][ny][nx] and u [3][nz_l][ny][nx] (fp64).  Fills
- * the halo ghost planes.  Returns after the device work is enqueued and the
- * host buffers have been consumed. */
+ * the halo ghost planes: with ghost-plane exchange (world > 1, or a non-AUTO
+ * halo) this is collective -- every rank calls it, like step().  Returns after
+ * the device work is enqueued and the host buffers have been consumed. */
 int lbm_cuboid_init_fields(lbm_cuboid_t *h, const double *rho, const double *u);
 /* Same from DEVICE pointers (fp64, same layouts, on this rank's device). */
 int lbm_cuboid_init_fields_device(lbm_cuboid_t *h, const double *rho, const double *u);
 
 /* Advance nsteps time steps (pull-stream with wall rules, then collide),
- * asynchronously on the compute stream.  nsteps >= 0. */
+ * asynchronously on the compute stream.  nsteps >= 0.  Collective over the
+ * ranks of a z-slab decomposition (all ranks take the same steps). */
 int lbm_cuboid_step(lbm_cuboid_t *h, int64_t nsteps);
 
 /* Block until all enqueued work of the handle is complete; reports
@@ -216,7 +218,8 @@ int lbm_cuboid_get_macroscopic(lbm_cuboid_t *h, double *rho, double *u);
 int lbm_cuboid_get_macroscopic_device(lbm_cuboid_t *h, double *rho, double *u);
 
 /* Stored populations, HOST fp64 [27][nz_l][ny][nx], paper direction order.
- * set_populations also refreshes the halo ghost planes. */
+ * set_populations also refreshes the halo ghost planes (collective like
+ * init_fields). */
 int lbm_cuboid_get_populations(lbm_cuboid_t *h, double *f);
 /* Planes [z_begin, z_begin + n_planes) of the local slab only: HOST fp64
  * [27][n_planes][ny][nx], paper direction order. */
