@@ -20,6 +20,7 @@ VDIR = os.path.join(ROOT, "build", "variants")
 
 VARIANTS = {
     "base": [],
+    "b128m5": ["LBM_MINB=5"],
     "b128m6": ["LBM_MINB=6"],
     "b128m7": ["LBM_MINB=7"],
     "b128m8": ["LBM_MINB=8"],
