@@ -104,6 +104,7 @@ def test_random_problem_matches_oracle(P, i):
     steps = 13
     o.step(steps)
     g.step(steps)
+    g.sync()  # with the bounds-checked build (LBM_CUBOID_LIB=...lib_debug.so) this reports violations
     fo, fg = o.get_populations(), g.get_populations()
     g.close()
     assert np.all(np.isfinite(fg))
@@ -166,6 +167,8 @@ def test_random_problem_p2p_slabs_match_oracle(P, i):
             h.step(1)
             h.sync()
     o.step(steps)
+    for h in hs:
+        h.sync()
     fg = np.concatenate([h.get_populations() for h in hs], axis=1)
     for h in hs:
         h.close()
