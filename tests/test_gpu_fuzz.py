@@ -4,9 +4,14 @@ correction mode, collision model, storage precision, launch mode, streaming
 pattern, halo mode: in-kernel wrap, NCCL send-to-self, self-P2P) through the C ABI against the CPU oracle, element by
 element, after a few steps from non-equilibrium populations.
 
-Bars as in test_gpu_parity.py: fp64 max|df| <= 1e-12; fp32 storage
-max|df|/|f| <= 1e-5 (reading R12).  The configurations come from PCG64(2107)
-so every run checks the same cases."""
+Bars: fp64 max|df| <= 1e-12 max(1, max|f|); fp32 storage max|df| <= 1e-5 max|f|.
+Random draws (small cs2 against large c^2, strong non-equilibrium) can make some
+populations tiny or even negative, where the per-population relative metric of
+reading R12 is ill-conditioned (fp32 rounding of the large populations, ~1e-7 of
+max|f|, divided by a population of 1e-5); the curated parity tests of
+test_gpu_parity.py keep R12 on the paper's configurations, and these bars scale
+with the population magnitude instead.  The configurations come from
+PCG64(2107) so every run checks the same cases (LBM_FUZZ_CASES sets how many)."""
 import numpy as np
 import pytest
 
@@ -14,7 +19,9 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-N_CASES = 200
+import os
+
+N_CASES = int(os.environ.get("LBM_FUZZ_CASES", "200"))  # more for a one-off stress run
 PER, BB, MW, FS = 0, 1, 2, 3
 
 
@@ -28,6 +35,15 @@ def P():
 
     P.load()
     return P
+
+
+def _assert_close(fg, fo, precision, info):
+    scale = np.abs(fo).max()
+    err = np.abs(fg - fo).max()
+    if precision == 0:
+        assert err <= 1e-12 * max(1.0, scale), (err, scale, info)
+    else:
+        assert err <= 1e-5 * scale, (err, scale, info)
 
 
 def _draw(rng):
@@ -108,12 +124,7 @@ def test_random_problem_matches_oracle(P, i):
     fo, fg = o.get_populations(), g.get_populations()
     g.close()
     assert np.all(np.isfinite(fg))
-    if kw["precision"] == 0:
-        err = np.abs(fg - fo).max()
-        assert err <= 1e-12, (err, kw, gpu)
-    else:
-        err = (np.abs(fg - fo) / np.abs(fo)).max()
-        assert err <= 1e-5, (err, kw, gpu)
+    _assert_close(fg, fo, kw["precision"], (kw, gpu))
 
 
 N_SLAB_CASES = 40
@@ -173,9 +184,4 @@ def test_random_problem_p2p_slabs_match_oracle(P, i):
     for h in hs:
         h.close()
     fo = o.get_populations()
-    if kw["precision"] == 0:
-        err = np.abs(fg - fo).max()
-        assert err <= 1e-12, (err, kw, world)
-    else:
-        err = (np.abs(fg - fo) / np.abs(fo)).max()
-        assert err <= 1e-5, (err, kw, world)
+    _assert_close(fg, fo, kw["precision"], (kw, world))
