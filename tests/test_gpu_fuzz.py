@@ -127,7 +127,7 @@ def test_random_problem_matches_oracle(P, i):
     _assert_close(fg, fo, kw["precision"], (kw, gpu))
 
 
-N_SLAB_CASES = 40
+N_SLAB_CASES = int(os.environ.get("LBM_FUZZ_SLAB_CASES", "40"))
 
 
 def _slab_cases():
