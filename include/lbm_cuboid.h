@@ -137,6 +137,10 @@ typedef struct {
   void *stream;                /* cudaStream_t for all compute work; NULL -> library-owned stream */
   void *buf_a, *buf_b;         /* optional caller-owned device buffers of lbm_cuboid_buffer_bytes()
                                   bytes each (e.g. torch tensors); NULL -> library cudaMalloc */
+  int32_t check_every;         /* > 0: every check_every steps step() enqueues the stability check of
+                                  lbm_cuboid_check (NaN, rho <= 0, |u| > 1) without blocking; a
+                                  failure is returned as LBM_EUNSTABLE, with the step, by a later
+                                  step() or by lbm_cuboid_sync().  0: off (default) */
 } lbm_cuboid_params;
 
 typedef struct lbm_cuboid lbm_cuboid_t;

@@ -119,6 +119,11 @@ struct lbm_cuboid {
   double* stage = nullptr;
   size_t stage_bytes = 0;
   double* d_check = nullptr;
+  // opt-in stability watch (params.check_every): the check of step watch_step
+  // lands in pinned host memory and is looked at by the next step()/sync()
+  double* h_watch = nullptr;
+  cudaEvent_t ev_watch = nullptr;
+  int64_t watch_step = -1;
   unsigned int* d_dbg = nullptr;  // bounds-check flag (written only by LBM_DEBUG_BOUNDS builds)
   int64_t launches = 0, cs_launches = 0, steps = 0;
   // CUDA graphs of kGraphSteps steps, one per starting buffer
@@ -165,6 +170,7 @@ int validate(const lbm_cuboid_params* p) {
   if (p->graphs < 0 || p->graphs > 3) return fail(LBM_EINVAL, "graphs must be 0, 1, 2 or 3");
   if (p->model < 0 || p->model > 1) return fail(LBM_EINVAL, "model must be an lbm_model");
   if (p->streaming < 0 || p->streaming > 1) return fail(LBM_EINVAL, "streaming must be an lbm_streaming");
+  if (p->check_every < 0) return fail(LBM_EINVAL, "check_every must be >= 0");
   if (p->streaming == LBM_STREAM_AA) {
     if (p->world > 1 || p->halo != LBM_HALO_AUTO)
       return fail(LBM_ENOTSUP, "AA in-place streaming is single-GPU only (no ghost-plane exchange)");
@@ -976,6 +982,10 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   for (int i = 0; i < nbuf; ++i)
     if (cudaMemsetAsync(h->buf[i], 0, bytes, h->stream) != cudaSuccess)
       return bail(fail(LBM_ECUDA, "cudaMemsetAsync failed"));
+  if (p->check_every > 0 &&
+      (cudaHostAlloc(&h->h_watch, 8 * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
+       cudaEventCreateWithFlags(&h->ev_watch, cudaEventDisableTiming) != cudaSuccess))
+    return bail(fail(LBM_ENOMEM, "pinned host memory / event for check_every"));
   // check(): 8 result slots + 8 partials per reduction block
   if (cudaMalloc(&h->d_check, size_t(8) * (1 + lbm::kCheckMaxBlocks) * sizeof(double)) != cudaSuccess)
     return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
@@ -1063,12 +1073,83 @@ int lbm_cuboid_init_fields(lbm_cuboid_t* h, const double* rho, const double* u) 
   return exchange(h, h->cur);
 }
 
+namespace {
+
+// the stability reduction of lbm_cuboid_check into h->d_check[0..6] (enqueued)
+int enqueue_check(lbm_cuboid* h) {
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->p.device));
+  const int64_t nodes = h->nxy * h->nzl;
+  const int nb = int(std::max<int64_t>(1, std::min<int64_t>({(nodes + lbm::kCheckThreads - 1) / lbm::kCheckThreads,
+                                                            int64_t(8) * sms, int64_t(lbm::kCheckMaxBlocks)})));
+  double* partial = h->d_check + 8;
+  if (h->p.precision == LBM_FP64)
+    lbm::k_check<double><<<nb, lbm::kCheckThreads, 0, h->stream>>>((const double*)h->buf[h->cur], partial, h->c,
+                                                                   aa_mode(h));
+  else
+    lbm::k_check<float><<<nb, lbm::kCheckThreads, 0, h->stream>>>((const float*)h->buf[h->cur], partial, h->c,
+                                                                  aa_mode(h));
+  CU(cudaGetLastError());
+  lbm::k_check_final<<<1, lbm::kCheckThreads, 0, h->stream>>>(partial, nb, h->d_check);
+  CU(cudaGetLastError());
+  h->launches += 2;
+  return LBM_OK;
+}
+
+// check_every: result of the pending watch (wait: block until it has landed)
+int poll_watch(lbm_cuboid* h, bool wait) {
+  if (h->watch_step < 0) return LBM_OK;
+  if (wait) {
+    CU(cudaEventSynchronize(h->ev_watch));
+  } else {
+    const cudaError_t e = cudaEventQuery(h->ev_watch);
+    if (e == cudaErrorNotReady) return LBM_OK;
+    CU(e);
+  }
+  const int64_t at = h->watch_step;
+  h->watch_step = -1;
+  if (h->h_watch[6] > 0)
+    return fail(LBM_EUNSTABLE, "check_every: %.0f nodes with NaN, rho <= 0 or |u| > 1 at step %lld", h->h_watch[6],
+                (long long)at);
+  return LBM_OK;
+}
+
+int enqueue_watch(lbm_cuboid* h) {
+  int rc;
+  if ((rc = poll_watch(h, true))) return rc;  // the previous one (check_every steps ago)
+  if ((rc = enqueue_check(h))) return rc;
+  CU(cudaMemcpyAsync(h->h_watch, h->d_check, 7 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CU(cudaEventRecord(h->ev_watch, h->stream));
+  h->watch_step = h->steps;
+  return LBM_OK;
+}
+
+int advance(lbm_cuboid* h, int64_t nsteps);
+
+}  // namespace
+
 int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   NvtxRange nv("lbm_cuboid_step");
   if (nsteps < 0) return fail(LBM_EINVAL, "nsteps must be >= 0");
   int rc = set_device(h);
   if (rc) return rc;
+  if ((rc = poll_watch(h, false))) return rc;
+  const int64_t K = h->p.check_every;
+  if (K <= 0) return advance(h, nsteps);
+  while (nsteps > 0) {
+    const int64_t n = std::min<int64_t>(nsteps, K - h->steps % K);
+    if ((rc = advance(h, n))) return rc;
+    nsteps -= n;
+    if (h->steps % K == 0 && (rc = enqueue_watch(h))) return rc;
+  }
+  return LBM_OK;
+}
+
+namespace {
+
+int advance(lbm_cuboid* h, int64_t nsteps) {
+  int rc;
   if (use_persistent(h)) return launch_persistent(h, nsteps);
   if (use_graphs(h)) {
     while (nsteps >= kGraphSteps) {
@@ -1088,6 +1169,8 @@ int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
   return LBM_OK;
 }
 
+}  // namespace
+
 int lbm_cuboid_sync(lbm_cuboid_t* h) {
   if (!h) return fail(LBM_EINVAL, "NULL handle");
   int rc = set_device(h);
@@ -1100,7 +1183,7 @@ int lbm_cuboid_sync(lbm_cuboid_t* h) {
   CU(cudaMemcpy(&flag, h->d_dbg, sizeof(flag), cudaMemcpyDeviceToHost));
   if (flag) return fail(LBM_ECUDA, "bounds check: a collide-stream kernel accessed outside its buffer");
 #endif
-  return LBM_OK;
+  return poll_watch(h, true);
 }
 
 int lbm_cuboid_get_macroscopic_device(lbm_cuboid_t* h, double* rho, double* u) {
@@ -1192,22 +1275,7 @@ int lbm_cuboid_check(lbm_cuboid_t* h, double out[7]) {
   if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
   int rc = set_device(h);
   if (rc) return rc;
-  int sms = 0;
-  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->p.device));
-  const int64_t nodes = h->nxy * h->nzl;
-  const int nb = int(std::max<int64_t>(1, std::min<int64_t>({(nodes + lbm::kCheckThreads - 1) / lbm::kCheckThreads,
-                                                            int64_t(8) * sms, int64_t(lbm::kCheckMaxBlocks)})));
-  double* partial = h->d_check + 8;
-  if (h->p.precision == LBM_FP64)
-    lbm::k_check<double><<<nb, lbm::kCheckThreads, 0, h->stream>>>((const double*)h->buf[h->cur], partial, h->c,
-                                                                   aa_mode(h));
-  else
-    lbm::k_check<float><<<nb, lbm::kCheckThreads, 0, h->stream>>>((const float*)h->buf[h->cur], partial, h->c,
-                                                                  aa_mode(h));
-  CU(cudaGetLastError());
-  lbm::k_check_final<<<1, lbm::kCheckThreads, 0, h->stream>>>(partial, nb, h->d_check);
-  CU(cudaGetLastError());
-  h->launches += 2;
+  if ((rc = enqueue_check(h))) return rc;
   CU(cudaMemcpyAsync(out, h->d_check, 7 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   CU(cudaStreamSynchronize(h->stream));
   if (out[6] > 0) return fail(LBM_EUNSTABLE, "%.0f nodes with NaN, rho <= 0 or |u| > 1 after %lld steps", out[6],
@@ -1420,6 +1488,8 @@ int lbm_cuboid_destroy(lbm_cuboid_t* h) {
       if (h->buf[i]) cudaFree(h->buf[i]);
   if (h->stage) cudaFree(h->stage);
   if (h->d_check) cudaFree(h->d_check);
+  if (h->h_watch) cudaFreeHost(h->h_watch);
+  if (h->ev_watch) cudaEventDestroy(h->ev_watch);
   if (h->d_dbg) cudaFree(h->d_dbg);
   if (h->d_rho) cudaFree(h->d_rho);
   if (h->ev_rho) cudaEventDestroy(h->ev_rho);

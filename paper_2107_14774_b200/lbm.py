@@ -55,7 +55,7 @@ class Params(ctypes.Structure):
                 ("device", ctypes.c_int32), ("halo", ctypes.c_int32), ("graphs", ctypes.c_int32),
                 ("model", ctypes.c_int32), ("streaming", ctypes.c_int32),
                 ("nccl_uid", ctypes.c_void_p), ("stream", ctypes.c_void_p),
-                ("buf_a", ctypes.c_void_p), ("buf_b", ctypes.c_void_p)]
+                ("buf_a", ctypes.c_void_p), ("buf_b", ctypes.c_void_p), ("check_every", ctypes.c_int32)]
 
 
 _lib = None
@@ -120,7 +120,7 @@ def _check(rc):
 
 def make_params(nx, ny, nz, r, s, cs2=0.0, omega_nu=1.0, omega_xi=1.0, omega_1=1.0, omega_high=1.0,
                 force=(0.0, 0.0, 0.0), bc=(0,) * 6, wall_u=0.0, corrections=0, precision=0,
-                rank=0, world=1, device=0, halo=0, graphs=0, model=0, streaming=0) -> Params:
+                rank=0, world=1, device=0, halo=0, graphs=0, model=0, streaming=0, check_every=0) -> Params:
     p = Params()
     load().lbm_cuboid_default_params(ctypes.byref(p))
     p.nx, p.ny, p.nz = int(nx), int(ny), int(nz)
@@ -137,6 +137,7 @@ def make_params(nx, ny, nz, r, s, cs2=0.0, omega_nu=1.0, omega_xi=1.0, omega_1=1
     p.graphs = int(graphs)
     p.model = int(model)
     p.streaming = int(streaming)
+    p.check_every = int(check_every)
     return p
 
 
@@ -175,14 +176,14 @@ class Lattice:
     def __init__(self, nx, ny, nz, r, s, cs2=0.0, omega_nu=1.0, omega_xi=1.0, omega_1=1.0,
                  omega_high=1.0, force=(0.0, 0.0, 0.0), bc=(0,) * 6, wall_u=0.0, corrections=0,
                  precision=0, rank=0, world=1, device=0, halo=0, graphs=0, model=0, streaming=0,
-                 nccl_uid: bytes | None = None, stream=None):
+                 nccl_uid: bytes | None = None, stream=None, check_every=0):
         import torch  # noqa: PLC0415  (device memory / streams only)
 
         L = load()
         self._torch = torch
         self.p = make_params(nx, ny, nz, r, s, cs2, omega_nu, omega_xi, omega_1, omega_high, force,
                              bc, wall_u, corrections, precision, rank, world, device, halo, graphs, model,
-                             streaming)
+                             streaming, check_every)
         self.nx, self.ny, self.nz = int(nx), int(ny), int(nz)
         self.world, self.rank = int(world), int(rank)
         self.nzl = self.nz // self.world

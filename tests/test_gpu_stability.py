@@ -59,3 +59,29 @@ def test_linear_instability_rate_matches_analysis(P):
     cs2 = synth.auto_cs2(1.0, 2.0)
     b1, b2 = _amplitudes(P, synth.omega_from_nu(0.01, cs2))
     assert b2 < b1 < 1e-6
+
+
+def test_check_every_reports_the_blow_up(P):
+    """params.check_every (SURVEY §5 failure detection): the config-1 run with
+    omega_xi = 1 blows up (see above); with check_every = 500 a later step() or
+    sync() returns LBM_EUNSTABLE naming the step of the first failed check,
+    without blocking the stepping in between.  The stable setting passes."""
+    w = synth.CONFIGS["tgv"].scaled(omega_xi=1.0)
+    g = P.Lattice(check_every=500, **w.params())
+    rho, u = synth.initial_fields(w)
+    g.init_fields(rho, u)
+    with pytest.raises(P.LbmError) as e:
+        for _ in range(40):
+            g.step(500)
+        g.sync()
+    assert e.value.code == P.lbm.LBM_EUNSTABLE and "at step" in str(e.value)
+    step = int(str(e.value).split("at step")[1].split()[0])
+    assert 5000 < step <= 20000 and step % 500 == 0
+    g.close()
+    cs2 = synth.auto_cs2(1.0, 2.0)
+    w2 = synth.CONFIGS["tgv"].scaled(omega_xi=synth.omega_from_nu(0.01, cs2))
+    g2 = P.Lattice(check_every=500, **w2.params())
+    g2.init_fields(rho, u)
+    g2.step(20000)
+    g2.sync()
+    g2.close()
