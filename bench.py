@@ -171,9 +171,23 @@ def host_cpu():
     return model, os.cpu_count()
 
 
+class pinned_to_one_core:
+    """Run the single-threaded oracle pinned to one host core."""
+
+    def __enter__(self):
+        self.prev = os.sched_getaffinity(0)
+        self.core = max(self.prev)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.prev)
+
+
 def oracle_mlups(w, budget_s=15.0, grid=(64, 64, 32), max_steps=None):
-    """The CPU oracle as it stands (single thread), on a bounded sample of the
-    workload: same physics on a smaller grid, as many steps as fit in budget_s."""
+    """The CPU oracle as it stands (single thread, pinned to one core), on a
+    bounded sample of the workload: same physics on a smaller grid, as many
+    steps as fit in budget_s."""
     import oracle as O
 
     nx, ny, nz = grid
@@ -181,14 +195,15 @@ def oracle_mlups(w, budget_s=15.0, grid=(64, 64, 32), max_steps=None):
     o = O.Oracle(**ws.params())
     rho, u = synth.initial_fields(ws)
     o.init_fields(rho, u)
-    t0 = time.perf_counter()
-    n = 0
-    while True:
-        o.step(1)
-        n += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s or (max_steps and n >= max_steps):
-            break
+    with pinned_to_one_core():
+        t0 = time.perf_counter()
+        n = 0
+        while True:
+            o.step(1)
+            n += 1
+            el = time.perf_counter() - t0
+            if el >= budget_s or (max_steps and n >= max_steps):
+                break
     return ws.nodes * n / el / 1e6, n, ws
 
 
@@ -205,14 +220,15 @@ def run_reference(args):
     o = O.Oracle(**ws.params())
     rho, u = synth.initial_fields(ws)
     o.init_fields(rho, u)
-    for _ in range(warm):
-        o.step(1)
-    t0 = time.perf_counter()
-    for _ in range(steps):
-        o.step(1)
-    el = time.perf_counter() - t0
+    with pinned_to_one_core():
+        for _ in range(warm):
+            o.step(1)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            o.step(1)
+        el = time.perf_counter() - t0
     v = ws.nodes * steps / el / 1e6
-    sample = f"oracle on {ws.nx}x{ws.ny}x{ws.nz} (same physics as {w.name}), {steps} steps, 1 thread"
+    sample = f"oracle on {ws.nx}x{ws.ny}x{ws.nz} (same physics as {w.name}), {steps} steps, 1 thread pinned to 1 core"
     line = {"metric": METRIC, "value": v, "unit": "MLUPS", "n_gpus": world, "steps": steps, "warmup": warm,
             "ms_per_step": el / steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
@@ -388,7 +404,7 @@ def run_cuda(args):
     if world == 1 and not args.no_cpu_baseline:
         v, n, ws = oracle_mlups(w, budget_s=12.0)
         cpu = {"value": v, "unit": "MLUPS", "cores": 1, "kind": "oracle",
-               "sample": f"{n} steps of {ws.nx}x{ws.ny}x{ws.nz} (same physics as {w.name}), single thread",
+               "sample": f"{n} steps of {ws.nx}x{ws.ny}x{ws.nz} (same physics as {w.name}), single thread pinned to 1 core",
                "cpu_model": host_cpu()[0], "host_logical_cores": host_cpu()[1]}
     line = {"metric": METRIC, "value": mlups, "unit": "MLUPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
