@@ -32,7 +32,8 @@
  * f~), R5 (lid augmentation on every link whose source crosses the +y face),
  * R6 (a wall wins over periodicity), R7 (free-slip = halfway specular
  * reflection), R8 (init f~ = f^eq(rho0, u0 + F/(2 rho0))), R16 (FULL_FD: the
- * isotropic lattice gradient of the same-time density).
+ * isotropic lattice gradient of the same-time density, mirror-image neighbours
+ * across walls).
  *
  * Parity pins: tests/test_oracle_*.py (closed forms, paper-printed appendices
  * and Eq. 69, conservation, SRT limit, order of the corrections (slope 3 on the
@@ -621,8 +622,11 @@ static double pull(const oracle_ctx *c, const double *fs, int x, int y, int z, i
 /* Isotropic second-order density gradient (reading R16):
  *   d_d rho(x) = (1/cs2) sum_a w_a e_ad rho(x + e_a),
  * w_a the cuboid rest weights (f^eq at rho = 1, u = 0), which satisfy
- * sum_a w_a e_a e_a = cs2 I.  A neighbour across a wall takes rho of the node
- * itself (zero normal gradient); periodic faces wrap. */
+ * sum_a w_a e_a e_a = cs2 I.  A neighbour across a wall face is the mirror
+ * image of that neighbour in the halfway wall, i.e. the node x + e_a with the
+ * crossed components of e_a set to zero (a zero-normal-gradient ghost: the
+ * wall-parallel gradient of a field linear along the wall stays exact);
+ * periodic faces wrap. */
 void oracle_density_gradient(const oracle_ctx *c, const double *rho, int x, int y, int z, double *g) {
   const oracle_params *p = &c->p;
   double w[NQ], u0[3] = {0.0, 0.0, 0.0};
@@ -631,16 +635,14 @@ void oracle_density_gradient(const oracle_ctx *c, const double *rho, int x, int 
   g[0] = g[1] = g[2] = 0.0;
   for (int a = 0; a < NQ; ++a) {
     int e[3] = {EX[a], EY[a], EZ[a]}, nb[3];
-    int wall = 0;
     for (int d = 0; d < 3; ++d) {
       nb[d] = xyz[d] + e[d];
       if (nb[d] < 0 || nb[d] >= n[d]) {
         int face = (nb[d] < 0) ? 2 * d : 2 * d + 1;
-        if (p->bc[face] != BC_PERIODIC) wall = 1;
-        nb[d] = wrap(nb[d], n[d]);
+        nb[d] = (p->bc[face] != BC_PERIODIC) ? xyz[d] : wrap(nb[d], n[d]);
       }
     }
-    double rn = wall ? rho[nid(p, x, y, z)] : rho[nid(p, nb[0], nb[1], nb[2])];
+    double rn = rho[nid(p, nb[0], nb[1], nb[2])];
     for (int d = 0; d < 3; ++d) g[d] += w[a] * c->e[a][d] * rn;
   }
   for (int d = 0; d < 3; ++d) g[d] /= p->cs2;

@@ -164,8 +164,9 @@ __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int
 // d_d rho = (1/cs2) sum_a w_a e_ad rho(x + e_a) (reading R16)
 // with the cuboid rest weights w_a = phi_x phi_y phi_z; per axis this is a central
 // difference 1/(2c) weighted by the rest weights of the two other axes.  A
-// neighbour across a wall face takes the node's own density.  rf has the
-// population-buffer plane structure: rf[(z_local + 1) * nxy + y * nx + x].
+// neighbour across a wall face is its mirror image in the halfway wall: the
+// offset along the crossed axes is zeroed (zero-normal-gradient ghost).  rf has
+// the population-buffer plane structure: rf[(z_local + 1) * nxy + y * nx + x].
 // rho_at(i, j, k) = density at offset (i-1, j-1, k-1) from the node (never
 // called for a neighbour across a wall); identical arithmetic for every source.
 template <class RhoAt>
@@ -175,7 +176,6 @@ __device__ __forceinline__ void density_gradient_g(const Consts& c, int x, int y
   const bool cx[3] = {x == 0 && is_wall(c.face[0]), false, x == c.nx - 1 && is_wall(c.face[1])};
   const bool cy[3] = {y == 0 && is_wall(c.face[2]), false, y == c.ny - 1 && is_wall(c.face[3])};
   const bool cz[3] = {z == 0 && is_wall(c.face[4]), false, z == c.nzl - 1 && is_wall(c.face[5])};
-  const double own = rho_at(1, 1, 1);
   double sx = 0.0, sy = 0.0, sz = 0.0;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
@@ -184,8 +184,7 @@ __device__ __forceinline__ void density_gradient_g(const Consts& c, int x, int y
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
         if (i == 1 && j == 1 && k == 1) continue;
-        const bool wall = cx[i] || cy[j] || cz[k];
-        const double v = wall ? own : rho_at(i, j, k);
+        const double v = rho_at(cx[i] ? 1 : i, cy[j] ? 1 : j, cz[k] ? 1 : k);
         if (i != 1) sx += (i == 2 ? 1.0 : -1.0) * c.phy[j] * c.phz[k] * v;
         if (j != 1) sy += (j == 2 ? 1.0 : -1.0) * c.phx[i] * c.phz[k] * v;
         if (k != 1) sz += (k == 2 ? 1.0 : -1.0) * c.phx[i] * c.phy[j] * v;

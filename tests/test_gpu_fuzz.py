@@ -4,14 +4,15 @@ correction mode, collision model, storage precision, launch mode, streaming
 pattern, halo mode: in-kernel wrap, NCCL send-to-self, self-P2P) through the C ABI against the CPU oracle, element by
 element, after a few steps from non-equilibrium populations.
 
-Bars: fp64 max|df| <= 1e-12 max(1, max|f|); fp32 storage max|df| <= 1e-5 max|f|.
-Random draws (small cs2 against large c^2, strong non-equilibrium) can make some
-populations tiny or even negative, where the per-population relative metric of
-reading R12 is ill-conditioned (fp32 rounding of the large populations, ~1e-7 of
-max|f|, divided by a population of 1e-5); the curated parity tests of
-test_gpu_parity.py keep R12 on the paper's configurations, and these bars scale
-with the population magnitude instead.  The configurations come from
-PCG64(2107) so every run checks the same cases (LBM_FUZZ_CASES sets how many)."""
+Bars: fp64 max|df| <= 1e-12 (north_star); fp32 storage the per-population
+relative metric of reading R12 with a floor,
+|df| <= 1e-5 max(|f_o|, 1e-2 max|f_o|) element by element.  Random draws (small
+cs2 against large c^2, strong non-equilibrium) can make single populations tiny
+or negative; there R12 alone divides the fp32 rounding of the large populations
+(~6e-8 of max|f| per stored value) by a near-zero population, and the floor
+keeps the bar at 1e-7 max|f| (about two fp32 ulps of the largest population).
+The configurations come from PCG64(2107) so every run checks the same cases
+(LBM_FUZZ_CASES sets how many)."""
 import numpy as np
 import pytest
 
@@ -38,12 +39,14 @@ def P():
 
 
 def _assert_close(fg, fo, precision, info):
-    scale = np.abs(fo).max()
-    err = np.abs(fg - fo).max()
+    err = np.abs(fg - fo)
     if precision == 0:
-        assert err <= 1e-12 * max(1.0, scale), (err, scale, info)
+        assert err.max() <= 1e-12, (err.max(), info)
     else:
-        assert err <= 1e-5 * scale, (err, scale, info)
+        # R12 with a floor at 1e-2 of the largest population
+        denom = np.maximum(np.abs(fo), 1e-2 * np.abs(fo).max())
+        rel = (err / denom).max()
+        assert rel <= 1e-5, (rel, err.max(), info)
 
 
 def _draw(rng):
