@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define LBM_CUBOID_ABI_VERSION 1
+#define LBM_CUBOID_ABI_VERSION 2
 
 typedef enum {
   LBM_OK = 0,
@@ -49,7 +49,13 @@ typedef enum {
   LBM_ECUDA = -3,     /* CUDA runtime error (message has the CUDA string) */
   LBM_ENCCL = -4,     /* NCCL error */
   LBM_EUNSTABLE = -5, /* NaN, rho <= 0 or |u| > 1 seen by lbm_cuboid_check() */
-  LBM_ENOTSUP = -6    /* unsupported parameter combination (e.g. AA streaming on several GPUs) */
+  LBM_ESINGULAR = -6, /* singular strain-rate system of the corrections (determinant of
+                         the 3x3 system of P:L1199-1203, Eq. 65): at create for the fluid at rest, or
+                         in flight at some node, where |D| or the back-substitution denominators
+                         |C_sy|, |C_sz| fell below 1e-12 rho cs2 (the C's grow the -3u^2/2 terms of
+                         P:L1194-1196); reported by lbm_cuboid_sync() and lbm_cuboid_check() after
+                         the step that saw it (DESIGN reading R17) */
+  LBM_ENOTSUP = -7    /* unsupported parameter combination (e.g. AA streaming on several GPUs) */
 } lbm_status;
 
 /* Face boundary types.  Faces are ordered -x, +x, -y, +y, -z, +z.  Opposite
@@ -191,8 +197,9 @@ int lbm_cuboid_p2p_connect(lbm_cuboid_t *h, const void *blob_down, const void *b
 /* Write a fresh 128-byte ncclUniqueId into out (call on rank 0 only). */
 int lbm_cuboid_nccl_unique_id(void *out128);
 
-/* Validate p (errors: LBM_EINVAL with a message naming the field, also for a
- * strain-rate system of the corrections that is singular at rest;
+/* Validate p (errors: LBM_EINVAL with a message naming the field;
+ * LBM_ESINGULAR for a strain-rate system of the corrections that is singular
+ * at rest;
  * LBM_ENOTSUP for unsupported mode combinations), bind the
  * device, allocate/bind buffers, upload the parameter block and, if needed,
  * create the NCCL communicator (collective over all ranks). */
@@ -213,7 +220,9 @@ int lbm_cuboid_init_fields_device(lbm_cuboid_t *h, const double *rho, const doub
 int lbm_cuboid_step(lbm_cuboid_t *h, int64_t nsteps);
 
 /* Block until all enqueued work of the handle is complete; reports
- * asynchronous CUDA/NCCL failures. */
+ * asynchronous CUDA/NCCL failures, LBM_ESINGULAR if a node's strain-rate
+ * system was singular during the steps since the last report (the steps still
+ * ran; the flag is cleared once reported), and a failed check_every watch. */
 int lbm_cuboid_sync(lbm_cuboid_t *h);
 
 /* rho [nz_l][ny][nx] and u [3][nz_l][ny][nx] (fp64) of the stored state into
@@ -233,7 +242,8 @@ int lbm_cuboid_set_populations(lbm_cuboid_t *h, const double *f);
 /* Rank-local reductions of the stored state, fp64:
  * out[0] = sum rho, out[1..3] = sum rho u, out[4] = sum rho |u|^2 / 2,
  * out[5] = max |u|, out[6] = number of nodes with NaN/Inf, rho <= 0 or |u| > 1.
- * Synchronises.  Returns LBM_EUNSTABLE if out[6] > 0. */
+ * Synchronises.  Returns LBM_EUNSTABLE if out[6] > 0, else LBM_ESINGULAR if
+ * the singular-system flag is set (see lbm_cuboid_sync). */
 int lbm_cuboid_check(lbm_cuboid_t *h, double out[7]);
 
 /* Replace the body force (e.g. time-periodic forcing); takes effect for the

@@ -76,6 +76,9 @@ def lib():
         L.oracle_run.argtypes = [ctypes.c_void_p, _D, _D, ctypes.c_int64]
         L.oracle_init.argtypes = [ctypes.c_void_p, _D, _D, _D]
         L.oracle_macroscopic.argtypes = [ctypes.c_void_p, _D, _D, _D]
+        L.oracle_singular_count.restype = ctypes.c_int64
+        L.oracle_singular_count.argtypes = []
+        L.oracle_singular_reset.argtypes = []
         _lib = L
     return _lib
 
@@ -144,6 +147,15 @@ def raw_source(u, F):
     phi = np.zeros(27)
     lib().oracle_raw_source(_p(_arr(u, 3)), _p(_arr(F, 3)), _p(phi))
     return phi
+
+
+def singular_count(reset=False):
+    """Nodes whose strain-rate system was singular (reading R17)
+    since the last reset."""
+    n = int(lib().oracle_singular_count())
+    if reset:
+        lib().oracle_singular_reset()
+    return n
 
 
 def raw_equilibria(rho, u, cs2):

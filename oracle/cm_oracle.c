@@ -298,6 +298,19 @@ void oracle_collide_raw_g(const oracle_ctx *c, const double *f, const double *gr
 
 void oracle_collide(const oracle_ctx *c, const double *f, double *ft) { oracle_collide_g(c, f, NULL, ft); }
 
+/* Singular strain-rate system (reading R17): a node whose
+ * closed-form denominators of P:L1199-1203 -- the determinant of the 3x3
+ * system in the printed d_x u_x, and C_sy, C_sz of the back-substitution --
+ * fall below 1e-12 rho cs2 in magnitude is counted here (the step still
+ * completes, as in the GPU path, which reports LBM_ESINGULAR). */
+static int64_t g_singular = 0;
+int64_t oracle_singular_count(void) { return g_singular; }
+void oracle_singular_reset(void) { g_singular = 0; }
+static void note_singular(double D, double Csy, double Csz, double rho, double cs2) {
+  const double thr = 1e-12 * rho * cs2;
+  if (fabs(D) < thr || fabs(Csy) < thr || fabs(Csz) < thr) g_singular++;
+}
+
 /* grad_rho: density gradient at the node for CORR_FULL_FD (NULL: zero). */
 void oracle_collide_g(const oracle_ctx *c, const double *f, const double *grad_rho, double *ft) {
   const oracle_params *p = &c->p;
@@ -355,6 +368,7 @@ void oracle_collide_g(const oracle_ctx *c, const double *f, const double *grad_r
     double Cby = (-2.0 * cs2 / wx + (3.0 * cs2 - r2) / 2.0 + g * 3.0 * uy * uy / 2.0) * rho;
     double Csz = (2.0 * cs2 / wn - (3.0 * cs2 - s2) / 2.0 - g * 3.0 * uz * uz / 2.0) * rho;
     double Cbz = (-2.0 * cs2 / wx + (3.0 * cs2 - s2) / 2.0 + g * 3.0 * uz * uz / 2.0) * rho;
+    note_singular(-Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx), Csy, Csz, rho, cs2);
     double dxux = (-Csz * Cby * Rs1 - Csy * (Cbz * Rs2 - Csz * Rb)) /
                   (-Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx));
     double dyuy = (Rs1 - Csx * dxux) / Csy;
@@ -489,6 +503,7 @@ void oracle_collide_raw_g(const oracle_ctx *c, const double *f, const double *gr
     double Cby = (-2.0 * cs2 / wx + (3.0 * cs2 - r2) / 2.0 + g * 3.0 * uy * uy / 2.0) * rho;
     double Csz = (2.0 * cs2 / wn - (3.0 * cs2 - s2) / 2.0 - g * 3.0 * uz * uz / 2.0) * rho;
     double Cbz = (-2.0 * cs2 / wx + (3.0 * cs2 - s2) / 2.0 + g * 3.0 * uz * uz / 2.0) * rho;
+    note_singular(-Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx), Csy, Csz, rho, cs2);
     double dxux = (-Csz * Cby * Rs1 - Csy * (Cbz * Rs2 - Csz * Rb)) /
                   (-Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx));
     double dyuy = (Rs1 - Csx * dxux) / Csy;

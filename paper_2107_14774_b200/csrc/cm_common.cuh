@@ -57,7 +57,19 @@ struct Consts {
   unsigned int nx_mul;        // fast division by nx (row of a plane index): see row_of()
   int nx_shift;
   unsigned int* dbg_flag;     // LBM_DEBUG_BOUNDS builds: set to 1 on an out-of-range access
+  unsigned int* sing_flag;    // set to 1 when a node's strain-rate system is singular (reading R17)
+  double sing_thr;            // 1e-12 cs2: threshold of the singular predicate on C/rho
+  double* aa_lid_rho;         // AA with the moving lid: rho of the lid-row nodes [z][x] (see k_aa)
 };
+
+// Singular strain-rate system (reading R17): the closed-form
+// denominators of P:L1199-1203 -- D, the determinant in the printed d_x u_x, and
+// C_sy, C_sz of the back-substitution -- below 1e-12 rho cs2 in magnitude.  The
+// kernels hold C/rho, so D = rho^3 det and C = rho (C/rho).  Rare: one flag word.
+__device__ __forceinline__ void note_singular(const Consts& c, double det, double Csy, double Csz, double rho) {
+  if (fabs(det) * (rho * rho) < c.sing_thr || fabs(Csy) < c.sing_thr || fabs(Csz) < c.sing_thr)
+    atomicOr(c.sing_flag, 1u);
+}
 
 // Row y = idx / nx of a plane index idx < 2^31 by multiply-high and shift
 // (round-up reciprocal, exact for 31-bit dividends; host side: fill_consts).

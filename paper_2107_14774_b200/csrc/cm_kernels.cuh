@@ -91,6 +91,14 @@ __device__ __forceinline__ double ring_rho(const T* src, const double* rf, const
     if (fk != FK_WRAP) return 0.0;
     p = (p < 0) ? c.nzl - 1 : 0;
   }
+  // a slab plane next to a ghost face: its pulled populations come partly from
+  // the ghost plane, which a neighbour overwrites concurrently with this launch
+  // (fused P2P halo: the neighbour's next step may start once this slab's
+  // boundary launch has published).  Its density is formed before this launch
+  // by the boundary-plane density pass (k_density / k_density_p2p), so read it
+  // from the density field and never touch the ghost planes here.
+  if ((p == 0 && c.face[4] == FK_GHOST) || (p == c.nzl - 1 && c.face[5] == FK_GHOST))
+    return __ldg(rf + (long long)(p + 1) * c.nxy + gy * c.nx + gx);
   double f[27];
   gather<T>(src, c, gx, gy, p, f);
   double r0 = 0.0;
@@ -139,6 +147,128 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T*
                                                    const double* __restrict__ rf, const __grid_constant__ Consts c,
                                                    int zbeg, int zstride) {
   collide_stream_ab<T, CORE_RAW, FD>(src, dst, rf, c, zbeg, zstride);
+}
+
+// ------------------------------------- x-pair kernel (fp32 storage, nx even)
+// One thread per pair of nodes (x, x + 1), x even, with 8-byte float2 loads and
+// stores (north_star: vectorised HBM access).  For direction q the pair's
+// sources in row R_q (plane z - e_z, row y - e_y, slot q) are
+//   e_x =  0: (R[x],     R[x + 1])  = the aligned pair P = R[x .. x+1]
+//   e_x = +1: (R[x - 1], R[x])      = (hi of lane-1's P, lo of P)
+//   e_x = -1: (R[x + 1], R[x + 2])  = (hi of P, lo of lane+1's P)
+// so a warp (32 pairs = 64 consecutive x of one row) issues ONE aligned 8-byte
+// load and at most one shuffle per direction; lane 0 / lane 31 fetch the one
+// value beyond the warp with a predicated scalar load (wrapped across a
+// periodic x face).  Rows and planes wrap periodically or address the ghost
+// planes as in gather().  A warp with any lane next to a wall, at the ragged
+// end of the plane, or whose x-neighbour pair sits on another row, gathers
+// each node with gather() instead.  Node x is
+// collided first and its 27 results are kept as fp32; node x + 1's collision
+// then stores each direction of both nodes as one float2.  The per-node
+// arithmetic, the loaded values and the stored values are exactly those of the
+// one-node-per-thread kernel, so the results are bitwise equal to it.
+template <typename T>
+struct StoreStash {  // node x: keep the rounded results until node x + 1's are known
+  float (&a)[27];
+  __device__ __forceinline__ void begin(double) {}
+  __device__ __forceinline__ void operator()(int q, double v) const { a[q] = (float)v; }
+};
+
+template <typename T>
+struct StorePair {  // node x + 1: store (node x, node x + 1) of direction q as one float2
+  float2* out;      // own pair of slot 0 (plane z)
+  int nxy2;         // nxy / 2 (float2 elements per slot)
+  const float (&a)[27];
+  const Consts* c;
+  const T* base;
+  __device__ __forceinline__ void begin(double) {}
+  __device__ __forceinline__ void operator()(int q, double v) const {
+    float2* p = out + q * nxy2;
+#ifdef LBM_DEBUG_BOUNDS
+    if ((unsigned long long)((const T*)p - base) + 1 >= (unsigned long long)c->buf_elems) {
+      atomicOr(c->dbg_flag, 1u);
+      return;
+    }
+#endif
+    __stcs(p, make_float2(a[q], (float)v));
+  }
+};
+
+#ifndef LBM_XP_MINB
+#define LBM_XP_MINB 4  // paper-rate kernel: resident 128-thread CTAs per SM requested from ptxas (<= 128 registers)
+#endif
+template <int KIND>
+__global__ void __launch_bounds__(kBlock, KIND == CORE_PAPER ? LBM_XP_MINB : 3) k_collide_stream_xpair(const float* __restrict__ src, float* __restrict__ dst,
+                                                     const __grid_constant__ Consts c, int zbeg, int zstride) {
+  const int npair = c.nxy >> 1;
+  const int pi = blockIdx.x * kBlock + threadIdx.x;
+  if (pi >= npair) return;
+  const int idx = 2 * pi;
+  const int y = row_of(c, idx);
+  const int x = idx - y * c.nx;  // even
+  const int z = zbeg + blockIdx.y * zstride;
+  const unsigned mask = __activemask();
+  const int lane = threadIdx.x & 31;
+  // pull sources of node x (rows and planes with periodic wrap or ghost planes)
+  const PullSrc<float> ps(src, c, x, y, z);
+  const bool wall = ps.wall || (c.has_walls && x + 1 == c.nx - 1 && c.face[1] >= FK_BOUNCE && c.face[1] <= FK_SLIP);
+  // a lane whose x-neighbour pair lies on another row (a warp spanning two
+  // rows) or beyond a periodic x face can use the shuffle only if it is the
+  // warp's first / last lane, which loads that value itself (wrapped in x)
+  const bool lane_ok = !wall && (x > 0 || lane == 0) && (x + 2 < c.nx || lane == 31);
+  const bool fast = (mask == 0xffffffffu) && __all_sync(mask, lane_ok);
+  float a[27];
+  double f[27];
+  float2* own = reinterpret_cast<float2*>(dst + (long long)(z + 1) * c.plane + idx);
+  const int nxy2 = c.nxy >> 1;
+  if (fast) {
+    // no lane next to a wall: every direction is one aligned float2 of row
+    // R_q = plane ps.pz[k], row ps.sy[j], slot q, plus one shuffle (e_x != 0)
+    const int xm = (x == 0) ? c.nx - 1 : x - 1;       // lane 0's extra source (e_x = +1)
+    const int xp2 = (x + 2 == c.nx) ? 0 : x + 2;      // lane 31's extra source (e_x = -1)
+    float v1[27];  // node x + 1
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const float* row = ps.pz[k] + ps.sy[j];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int q = LBM_Q(i, j, k);
+          const float* r = row + q * c.nxy;  // R_q
+          const float2 P = __ldg(reinterpret_cast<const float2*>(LBM_CHECK_LD(src, r + x, c)));
+          if (i == 1) {
+            a[q] = P.x;
+            v1[q] = P.y;
+          } else if (i == 2) {  // e_x = +1
+            float lo = __shfl_up_sync(0xffffffffu, P.y, 1);
+            if (lane == 0) lo = __ldg(LBM_CHECK_LD(src, r + xm, c));
+            a[q] = lo;
+            v1[q] = P.x;
+          } else {  // e_x = -1
+            float hi = __shfl_down_sync(0xffffffffu, P.x, 1);
+            if (lane == 31) hi = __ldg(LBM_CHECK_LD(src, r + xp2, c));
+            a[q] = P.y;
+            v1[q] = hi;
+          }
+        }
+      }
+#pragma unroll
+    for (int q = 0; q < 27; ++q) f[q] = (double)a[q];
+    StoreStash<float> s0{a};
+    run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, s0);
+#pragma unroll
+    for (int q = 0; q < 27; ++q) f[q] = (double)v1[q];
+    StorePair<float> s1{own, nxy2, a, &c, dst};
+    run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, s1);
+    return;
+  }
+  gather<float>(src, c, x, y, z, f);
+  StoreStash<float> s0{a};
+  run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, s0);
+  gather<float>(src, c, x + 1, y, z, f);
+  StorePair<float> s1{own, nxy2, a, &c, dst};
+  run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, s1);
 }
 
 // chunk blockIdx.z covers planes [z0, z1), z0 = zbeg + blockIdx.z * zstride,
@@ -392,9 +522,24 @@ __global__ void LBM_CS_BOUNDS k_aa(T* buf, const __grid_constant__ Consts c, int
     T* p = buf + (long long)(z + 1) * c.plane + idx;
 #pragma unroll
     for (int q = 0; q < 27; ++q) f[q] = ldg(LBM_CHECK_LD(buf, p + q * c.nxy, c));
-    StoreRev<T> st{buf, p, c.nxy, &c};
+    double* lid = (c.aa_lid_rho && y == c.ny - 1) ? c.aa_lid_rho + z * c.nx + x : nullptr;
+    StoreRev<T> st{buf, p, c.nxy, &c, lid, 0.0};
     run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, st);
   }
+}
+
+// AA with the moving lid, after init_fields / set_populations (layout R): the
+// density sum f~ of every lid-row node for the first odd step (see gather<REV>).
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_aa_lid_rho(const T* __restrict__ buf, const __grid_constant__ Consts c) {
+  const int x = blockIdx.x * kBlock + threadIdx.x;
+  if (x >= c.nx) return;
+  const int z = blockIdx.y;
+  const T* p = buf + (long long)(z + 1) * c.plane + (c.ny - 1) * c.nx + x;
+  double r0 = 0.0;  // sum f~_q in q order (layout R: slot 26 - q), as StoreRev forms it
+#pragma unroll
+  for (int q = 0; q < 27; ++q) r0 += ldg(p + (26 - q) * c.nxy);
+  c.aa_lid_rho[z * c.nx + x] = r0;
 }
 
 // Canonical post-collision populations f~_q(x) of node x from an AA buffer:

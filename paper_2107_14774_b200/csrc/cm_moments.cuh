@@ -109,6 +109,7 @@ __device__ __forceinline__ void second_order_diag(const Consts& c, double rho, d
     }
     const double t1 = Csx * Cbz - Csz * Cbx;
     const double det = -Csx * Csz * Cby - Csy * t1;
+    note_singular(c, det, Csy, Csz, rho);
     const double inv_det = 1.0 / det;
     const double dxux = (-Csz * Cby * Rs1 - Csy * (Cbz * Rs2 - Csz * Rb)) * inv_det;
     const double dyuy = (Csx * (Rs2 * Cbz - Csz * Rb) - Rs1 * t1) * inv_det;
@@ -405,7 +406,9 @@ __device__ __forceinline__ void collide_raw(const Consts& c, double (&f)[27], do
         Rs2 += (-lsx + lsz) * inv_rho;
       }
       const double t1 = Csx * Cbz - Csz * Cbx;
-      const double inv_det = 1.0 / (-Csx * Csz * Cby - Csy * t1);
+      const double det = -Csx * Csz * Cby - Csy * t1;
+      note_singular(c, det, Csy, Csz, rho);
+      const double inv_det = 1.0 / det;
       const double dxux = (-Csz * Cby * Rs1 - Csy * (Cbz * Rs2 - Csz * Rb)) * inv_det;
       const double dyuy = (Csx * (Rs2 * Cbz - Csz * Rb) - Rs1 * t1) * inv_det;
       const double dzuz = (Csx * Cby * (Rs1 - Rs2) - Csy * (Csx * Rb - Rs2 * Cbx)) * inv_det;

@@ -102,8 +102,17 @@ __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int
   const T* p0 = pz[1];
   double rho_f = 0.0;  // reading R4: rho_f = sum_b f~_b(x_f, t) at the wall-adjacent node
   if (cym == FK_MOVING) {
+    if (REV) {
+      // AA odd step: 26 of the node's 27 slots belong to the neighbour threads
+      // that pull from them and then push into them (the bijection of k_aa), so
+      // they may already be overwritten; rho_f = sum f~(x_f, t), formed by the
+      // even step that stored them (StoreRev), or by k_aa_lid_rho after
+      // init/set_populations, in the same q order as below
+      rho_f = c.aa_lid_rho[z * nx + x];
+    } else {
 #pragma unroll
-    for (int q = 0; q < 27; ++q) rho_f += ldg(LBM_CHECK_LD(src, p0 + q * c.nxy + own, c));
+      for (int q = 0; q < 27; ++q) rho_f += ldg(LBM_CHECK_LD(src, p0 + q * c.nxy + own, c));
+    }
   }
   if (!c.has_slip) {
     // no free-slip face (uniform branch): per direction either the plain pull or
@@ -185,9 +194,11 @@ __device__ __forceinline__ void density_gradient_g(const Consts& c, int x, int y
       for (int i = 0; i < 3; ++i) {
         if (i == 1 && j == 1 && k == 1) continue;
         const double v = rho_at(cx[i] ? 1 : i, cy[j] ? 1 : j, cz[k] ? 1 : k);
-        if (i != 1) sx += (i == 2 ? 1.0 : -1.0) * c.phy[j] * c.phz[k] * v;
-        if (j != 1) sy += (j == 2 ? 1.0 : -1.0) * c.phx[i] * c.phz[k] * v;
-        if (k != 1) sz += (k == 2 ? 1.0 : -1.0) * c.phx[i] * c.phy[j] * v;
+        // explicit fused multiply-adds: the same rounding in every kernel that
+        // inlines this, whatever the compiler's contraction choices
+        if (i != 1) sx = __fma_rn((i == 2 ? 1.0 : -1.0) * c.phy[j] * c.phz[k], v, sx);
+        if (j != 1) sy = __fma_rn((j == 2 ? 1.0 : -1.0) * c.phx[i] * c.phz[k], v, sy);
+        if (k != 1) sz = __fma_rn((k == 2 ? 1.0 : -1.0) * c.phx[i] * c.phy[j], v, sz);
       }
   gx = 0.5 * sx;
   gy = c.h1y * sy;
@@ -231,9 +242,17 @@ struct StoreRev {
   T* out;
   int nxy;
   const Consts* c;
-  __device__ __forceinline__ void begin(double) {}
-  __device__ __forceinline__ void operator()(int q, double v) const {
+  // lid-row node with the moving lid: rho_f = sum of its stored f~ in q order
+  // (what the two-buffer gather and k_aa_lid_rho sum), for the next odd step
+  double* lid_rho;
+  double acc;
+  __device__ __forceinline__ void begin(double) { acc = 0.0; }
+  __device__ __forceinline__ void operator()(int q, double v) {
     stcs<T>(LBM_CHECK_ST(base, out + (26 - q) * nxy, *c), v);
+    if (lid_rho) {
+      acc += (double)(T)v;
+      if (q == 26) *lid_rho = acc;
+    }
   }
 };
 

@@ -97,6 +97,7 @@ struct lbm_cuboid {
   bool fd = false;           // FULL_FD: density pass + isotropic gradient
   bool fd_fused = true;      // FULL_FD: fused 2.5D kernel (fp64) or density pass + collide (fp32);
                              // env LBM_FD_FUSED=0/1 forces the two-pass / fused path
+  bool xpair = false;        // fp32 storage, nx even: x-pair kernel (float2 loads/stores); opt-in LBM_XPAIR=1
   bool aa = false;           // AA in-place streaming: one buffer; cur = 0 layout R, cur = 1 layout N
   double* d_rho = nullptr;   // FULL_FD density field, population-buffer plane structure (ghost planes)
   cudaEvent_t ev_rho = nullptr;
@@ -124,7 +125,8 @@ struct lbm_cuboid {
   double* h_watch = nullptr;
   cudaEvent_t ev_watch = nullptr;
   int64_t watch_step = -1;
-  unsigned int* d_dbg = nullptr;  // bounds-check flag (written only by LBM_DEBUG_BOUNDS builds)
+  unsigned int* d_dbg = nullptr;  // [0] bounds-check flag (LBM_DEBUG_BOUNDS builds), [1] singular-system flag
+  double* d_aa_lid = nullptr;     // AA + moving lid: rho of the lid-row nodes (Consts::aa_lid_rho)
   int64_t launches = 0, cs_launches = 0, steps = 0;
   // CUDA graphs of kGraphSteps steps, one per starting buffer
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
@@ -190,11 +192,13 @@ int validate(const lbm_cuboid_params* p) {
     const double gx = 3.0 * cs2 - 1.0, gy = 3.0 * cs2 - p->r * p->r, gz = 3.0 * cs2 - p->s * p->s;
     const double Csx = -csn + 0.5 * gx, Cbx = -csx + 0.5 * gx, Csy = csn - 0.5 * gy, Cby = -csx + 0.5 * gy,
                  Csz = csn - 0.5 * gz, Cbz = -csx + 0.5 * gz;
+    // the in-flight predicate of reading R17 (note_singular) at rho = 1, u = 0; no
+    // valid (r, s, cs2, omega) was found where it holds at rest (DESIGN R17), so
+    // in practice the system only degenerates in flight, through the 3u^2/2 terms
     const double det = -Csx * Csz * Cby - Csy * (Csx * Cbz - Csz * Cbx);
-    const double scale = std::max({std::fabs(Csx), std::fabs(Csy), std::fabs(Csz), std::fabs(Cbx), std::fabs(Cby),
-                                   std::fabs(Cbz)});
-    if (!(std::fabs(det) > 1e-12 * scale * scale * scale))
-      return fail(LBM_EINVAL, "the strain-rate system of the corrections is singular at rest (det = %g) for these "
+    const double thr = 1e-12 * cs2;
+    if (!(std::fabs(det) >= thr && std::fabs(Csy) >= thr && std::fabs(Csz) >= thr))
+      return fail(LBM_ESINGULAR, "the strain-rate system of the corrections is singular at rest (det = %g) for these "
                   "r, s, cs2, omega_nu, omega_xi", det);
   }
   return LBM_OK;
@@ -260,6 +264,7 @@ void fill_consts(lbm_cuboid* h) {
     c.face[5] = kind(p.bc[5]);
   }
   c.buf_elems = h->buf_elems;
+  c.sing_thr = 1e-12 * cs2;
   // fast division by nx for idx < 2^31: m = ceil(2^p / nx), p = 31 + ceil(log2 nx),
   // idx / nx = umulhi(idx, m) >> (p - 32)  (nx = 1: no division)
   if (p.nx > 1) {
@@ -386,6 +391,14 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
       else LBM_FDF(float, lbm::CORE_GENERIC);
     }
 #undef LBM_FDF
+  } else if (h->xpair && !fp64 && !h->fd) {
+    const dim3 gp(unsigned((h->nxy / 2 + lbm::kBlock - 1) / lbm::kBlock), unsigned(nplanes), 1);
+    if (h->p.model == LBM_MODEL_RM)
+      lbm::k_collide_stream_xpair<lbm::CORE_RAW><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg, zstride);
+    else if (h->paper_rates)
+      lbm::k_collide_stream_xpair<lbm::CORE_PAPER><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg, zstride);
+    else
+      lbm::k_collide_stream_xpair<lbm::CORE_GENERIC><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg, zstride);
   } else if (h->p.model == LBM_MODEL_RM)
     LBM_LAUNCH(k_collide_stream_raw);
   else if (h->paper_rates)
@@ -778,6 +791,11 @@ int p2p_step(lbm_cuboid* h) {
     CU(cudaGetLastError());
     h->launches++;
     h->epoch++;
+    // the interior's fused FULL_FD kernel takes the density of planes 0 and
+    // nz_l - 1 from d_rho (ring_rho: it never reads the ghost planes, which the
+    // neighbours overwrite once this slab's boundary launch has published)
+    CU(cudaEventRecord(h->ev_rho, h->comm_stream));
+    CU(cudaStreamWaitEvent(h->stream, h->ev_rho, 0));
     if ((rc = p2p_wait(h))) return rc;
   }
   if ((rc = launch_cs(h, src, dst, 0, nb, std::max(1, h->nzl - 1), h->comm_stream, which, h->epoch + 1, false)))
@@ -818,6 +836,20 @@ template <typename T>
 int init_kernel(lbm_cuboid* h, const double* rho, const double* u, long long ustride, int zbeg, int n) {
   lbm::k_init<T><<<grid_for(h, n), lbm::kBlock, 0, h->stream>>>(rho, u, ustride, (T*)h->buf[h->cur], h->c, zbeg,
                                                                  h->aa ? 1 : 0);
+  CU(cudaGetLastError());
+  h->launches++;
+  return LBM_OK;
+}
+
+// AA with the moving lid: densities of the lid-row nodes of the stored layout-R
+// state (after init_fields / set_populations) for the first odd step
+int aa_lid_prep(lbm_cuboid* h) {
+  if (!h->d_aa_lid) return LBM_OK;
+  const dim3 g(unsigned((h->p.nx + lbm::kBlock - 1) / lbm::kBlock), unsigned(h->nzl), 1);
+  if (h->p.precision == LBM_FP64)
+    lbm::k_aa_lid_rho<double><<<g, lbm::kBlock, 0, h->stream>>>((const double*)h->buf[0], h->c);
+  else
+    lbm::k_aa_lid_rho<float><<<g, lbm::kBlock, 0, h->stream>>>((const float*)h->buf[0], h->c);
   CU(cudaGetLastError());
   h->launches++;
   return LBM_OK;
@@ -944,6 +976,10 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->fd_fused = (p->precision == LBM_FP64);
   if (const char* e = std::getenv("LBM_FD_FUSED")) h->fd_fused = (std::atoi(e) != 0);
   h->aa = (p->streaming == LBM_STREAM_AA);
+  // fp32 storage with an even nx (8-byte aligned node pairs): the x-pair kernel,
+  // opt-in (LBM_XPAIR=1): measured no faster than one node per thread
+  const char* xp = std::getenv("LBM_XPAIR");
+  h->xpair = (p->precision == LBM_FP32_STORAGE) && (p->nx % 2 == 0) && !h->aa && xp && std::atoi(xp) != 0;
   h->p2p = h->ghost && (p->halo == LBM_HALO_P2P);
   // the P2P step forms only the density planes the boundary collision needs
   // (k_density_p2p); its interior must be the fused kernel, which forms its own
@@ -989,10 +1025,17 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   // check(): 8 result slots + 8 partials per reduction block
   if (cudaMalloc(&h->d_check, size_t(8) * (1 + lbm::kCheckMaxBlocks) * sizeof(double)) != cudaSuccess)
     return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
-  if (cudaMalloc(&h->d_dbg, sizeof(unsigned int)) != cudaSuccess ||
-      cudaMemsetAsync(h->d_dbg, 0, sizeof(unsigned int), h->stream) != cudaSuccess)
+  if (cudaMalloc(&h->d_dbg, 2 * sizeof(unsigned int)) != cudaSuccess ||
+      cudaMemsetAsync(h->d_dbg, 0, 2 * sizeof(unsigned int), h->stream) != cudaSuccess)
     return bail(fail(LBM_ENOMEM, "cudaMalloc failed"));
   h->c.dbg_flag = h->d_dbg;
+  h->c.sing_flag = h->d_dbg + 1;
+  if (h->aa && p->bc[3] == LBM_BC_MOVING_WALL) {
+    const size_t lb = size_t(p->nx) * h->nzl * sizeof(double);
+    if (cudaMalloc(&h->d_aa_lid, lb) != cudaSuccess || cudaMemsetAsync(h->d_aa_lid, 0, lb, h->stream) != cudaSuccess)
+      return bail(fail(LBM_ENOMEM, "cudaMalloc(%zu) for the AA lid densities failed", lb));
+    h->c.aa_lid_rho = h->d_aa_lid;
+  }
   if (h->fd) {
     const size_t rb = size_t(h->nxy) * (h->nzl + 2) * sizeof(double);
     if (cudaMalloc(&h->d_rho, rb) != cudaSuccess || cudaMemsetAsync(h->d_rho, 0, rb, h->stream) != cudaSuccess)
@@ -1005,7 +1048,8 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
     cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
     if (cudaStreamCreateWithPriority(&h->comm_stream, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
         cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&h->ev_rho, cudaEventDisableTiming) != cudaSuccess)
       return bail(fail(LBM_ECUDA, "stream/event creation failed"));
     PfnWaitValue32 w32 = nullptr;
     if ((rc = driver_fn("cuStreamWaitValue32", &w32))) return bail(rc);
@@ -1048,6 +1092,7 @@ int lbm_cuboid_init_fields_device(lbm_cuboid_t* h, const double* rho, const doub
   if ((rc = wait_halo(h))) return rc;
   if (h->aa) h->cur = 0;  // AA: the canonical state is written in layout R
   if ((rc = run_init(h, rho, u, (long long)h->nzl * h->nxy, 0, h->nzl))) return rc;
+  if ((rc = aa_lid_prep(h))) return rc;
   return exchange(h, h->cur);
 }
 
@@ -1069,6 +1114,7 @@ int lbm_cuboid_init_fields(lbm_cuboid_t* h, const double* rho, const double* u) 
                          cudaMemcpyHostToDevice, h->stream));
     if ((rc = run_init(h, srho, su, (long long)cnt, z, n))) return rc;
   }
+  if ((rc = aa_lid_prep(h))) return rc;
   CU(cudaStreamSynchronize(h->stream));
   return exchange(h, h->cur);
 }
@@ -1126,6 +1172,23 @@ int enqueue_watch(lbm_cuboid* h) {
 
 int advance(lbm_cuboid* h, int64_t nsteps);
 
+// Device flag words after a synchronisation: the singular strain-rate predicate
+// (reading R17; reported once, then cleared) and, in
+// LBM_DEBUG_BOUNDS builds, the bounds check.
+int poll_flags(lbm_cuboid* h) {
+  unsigned int flag[2] = {0, 0};
+  CU(cudaMemcpy(flag, h->d_dbg, sizeof(flag), cudaMemcpyDeviceToHost));
+#ifdef LBM_DEBUG_BOUNDS
+  if (flag[0]) return fail(LBM_ECUDA, "bounds check: a collide-stream kernel accessed outside its buffer");
+#endif
+  if (flag[1]) {
+    CU(cudaMemset(h->d_dbg + 1, 0, sizeof(unsigned int)));
+    return fail(LBM_ESINGULAR, "singular strain-rate system at a node (|det| or |C_sy|, |C_sz| < 1e-12 rho cs2, "
+                "S:L207) in the steps before step %lld", (long long)h->steps);
+  }
+  return LBM_OK;
+}
+
 }  // namespace
 
 int lbm_cuboid_step(lbm_cuboid_t* h, int64_t nsteps) {
@@ -1178,11 +1241,7 @@ int lbm_cuboid_sync(lbm_cuboid_t* h) {
   if ((rc = wait_halo(h))) return rc;
   CU(cudaStreamSynchronize(h->stream));
   if (h->comm_stream) CU(cudaStreamSynchronize(h->comm_stream));
-#ifdef LBM_DEBUG_BOUNDS
-  unsigned int flag = 0;
-  CU(cudaMemcpy(&flag, h->d_dbg, sizeof(flag), cudaMemcpyDeviceToHost));
-  if (flag) return fail(LBM_ECUDA, "bounds check: a collide-stream kernel accessed outside its buffer");
-#endif
+  if ((rc = poll_flags(h))) return rc;
   return poll_watch(h, true);
 }
 
@@ -1268,6 +1327,7 @@ int lbm_cuboid_set_populations(lbm_cuboid_t* h, const double* f) {
     h->launches++;
     CU(cudaStreamSynchronize(h->stream));
   }
+  if ((rc = aa_lid_prep(h))) return rc;
   return exchange(h, h->cur);
 }
 
@@ -1280,7 +1340,7 @@ int lbm_cuboid_check(lbm_cuboid_t* h, double out[7]) {
   CU(cudaStreamSynchronize(h->stream));
   if (out[6] > 0) return fail(LBM_EUNSTABLE, "%.0f nodes with NaN, rho <= 0 or |u| > 1 after %lld steps", out[6],
                               (long long)h->steps);
-  return LBM_OK;
+  return poll_flags(h);
 }
 
 int lbm_cuboid_set_force(lbm_cuboid_t* h, const double force[3]) {
@@ -1491,6 +1551,7 @@ int lbm_cuboid_destroy(lbm_cuboid_t* h) {
   if (h->h_watch) cudaFreeHost(h->h_watch);
   if (h->ev_watch) cudaEventDestroy(h->ev_watch);
   if (h->d_dbg) cudaFree(h->d_dbg);
+  if (h->d_aa_lid) cudaFree(h->d_aa_lid);
   if (h->d_rho) cudaFree(h->d_rho);
   if (h->ev_rho) cudaEventDestroy(h->ev_rho);
   clear_timing(h);

@@ -18,7 +18,8 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # LBM_CUBOID_LIB selects an alternative build (kernel-variant sweeps); default in-tree
 LIB_PATH = os.environ.get("LBM_CUBOID_LIB", os.path.join(_PKG, "liblbm_cuboid.so"))
 
-LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EUNSTABLE, LBM_ENOTSUP = 0, -1, -2, -3, -4, -5, -6
+LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EUNSTABLE, LBM_ESINGULAR, LBM_ENOTSUP = (
+    0, -1, -2, -3, -4, -5, -6, -7)
 BC_PERIODIC, BC_BOUNCE_BACK, BC_MOVING_WALL, BC_FREE_SLIP = 0, 1, 2, 3
 CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF, CORR_FULL_FD = 0, 1, 2, 3
 FP64, FP32_STORAGE = 0, 1

@@ -268,3 +268,34 @@ def test_config5_geometry_64cubed_slabs_bitwise(P, world):
     f = _gather(hs)
     _close(hs)
     assert np.array_equal(f, f_ref)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("case", ["tgv_periodic", "cavity_walls"])
+def test_p2p_slabs_run_concurrently_within_a_step(P, case, world):
+    """The slabs' steps in flight together: every slab's step(1) is enqueued
+    before any is synchronised, so one slab's boundary kernel stores into its
+    neighbours' ghost planes and publishes its flag while the neighbours'
+    interior and boundary kernels run (4-8 streams on the GPU at once).  Every
+    flag wait is on the PREVIOUS step (host-synchronised between steps), so no
+    stream waits on another slab's work that is still queued behind it
+    (B200_PROFILING.md on ranks sharing a GPU).  Bitwise equal to the
+    undecomposed lattice; large enough planes that the launches overlap."""
+    w0, kw = CASES[case]
+    w = w0.scaled(nx=160, ny=96, nz=8 * world)
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 58)
+    ref = _lat(P, w, **kw)
+    ref.init_fields(rho, u)
+    ref.step(20)
+    f_ref = ref.get_populations()
+    ref.close()
+    hs = _slabs(P, w, world, **kw)
+    _split_init(hs, rho, u)
+    for _ in range(20):
+        for h in hs:
+            h.step(1)
+        for h in hs:
+            h.sync()
+    f = _gather(hs)
+    _close(hs)
+    assert np.array_equal(f, f_ref)
