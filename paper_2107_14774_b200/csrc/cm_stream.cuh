@@ -46,6 +46,15 @@ struct PullSrc {
   }
 };
 
+// is node (x, y, z) next to a wall face (bounce-back, moving or free-slip)?
+// (the predicate of PullSrc::wall)
+__device__ __forceinline__ bool wall_adjacent(const Consts& c, int x, int y, int z) {
+  if (!c.has_walls) return false;
+  auto w = [](int fk) { return fk >= FK_BOUNCE && fk <= FK_SLIP; };
+  return (x == 0 && w(c.face[0])) || (x == c.nx - 1 && w(c.face[1])) || (y == 0 && w(c.face[2])) ||
+         (y == c.ny - 1 && w(c.face[3])) || (z == 0 && w(c.face[4])) || (z == c.nzl - 1 && w(c.face[5]));
+}
+
 // REV (AA odd steps): the source buffer holds f~_s(z) at slot 26 - s of node z.
 template <typename T, bool REV = false>
 __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int y, int z, double (&f)[27]) {

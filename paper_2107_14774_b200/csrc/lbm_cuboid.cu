@@ -17,6 +17,7 @@
 //     compute stream: interior planes 1..nz_l-2 (concurrent) -> wait(halo stream)
 #include "../../include/lbm_cuboid.h"
 #include "cm_kernels.cuh"
+#include "cm_tma.cuh"
 
 #include <cuda.h>  // driver types only; entry points come from cudaGetDriverEntryPointByVersion
 #include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys (no-ops without a tool)
@@ -97,6 +98,9 @@ struct lbm_cuboid {
   bool fd = false;           // FULL_FD: density pass + isotropic gradient
   bool fd_fused = true;      // FULL_FD: fused 2.5D kernel (fp64) or density pass + collide (fp32);
                              // env LBM_FD_FUSED=0/1 forces the two-pass / fused path
+  bool tma = false;          // TMA-staged collide-stream kernel (cm_tma.cuh); opt-in LBM_TMA=1
+  lbm::TmaMaps tmaps[2];     // buf[i] as the 3D tensor (x, y, 27 (nz_l + 2)) for the TMA unit
+  int tma_grid = 0;          // persistent grid size of the TMA kernel (resident CTAs)
   bool xpair = false;        // fp32 storage, nx even: x-pair kernel (float2 loads/stores); opt-in LBM_XPAIR=1
   bool aa = false;           // AA in-place streaming: one buffer; cur = 0 layout R, cur = 1 layout N
   double* d_rho = nullptr;   // FULL_FD density field, population-buffer plane structure (ghost planes)
@@ -391,6 +395,25 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
       else LBM_FDF(float, lbm::CORE_GENERIC);
     }
 #undef LBM_FDF
+  } else if (h->tma && !h->fd) {
+    const int ntx = int((h->p.nx + lbm::kTmaTx - 1) / lbm::kTmaTx);
+    const lbm::TmaTiles tl{zbeg, zstride, nplanes, ntx, (long long)nplanes * h->p.ny * ntx};
+    const unsigned grid = unsigned(std::min<long long>(tl.count, h->tma_grid));
+    const lbm::TmaMaps& maps = h->tmaps[(src == h->buf[0]) ? 0 : 1];
+    const int kind = (h->p.model == LBM_MODEL_RM) ? lbm::CORE_RAW : (h->paper_rates ? lbm::CORE_PAPER : lbm::CORE_GENERIC);
+#define LBM_TMAK(T, K)                                                                                          \
+  lbm::k_collide_stream_tma<T, K><<<grid, lbm::kTmaThreads, lbm::tma_smem_bytes<T>(), s>>>(maps, (const T*)src, \
+                                                                                          (T*)dst, h->c, tl)
+    if (fp64) {
+      if (kind == lbm::CORE_PAPER) LBM_TMAK(double, lbm::CORE_PAPER);
+      else if (kind == lbm::CORE_RAW) LBM_TMAK(double, lbm::CORE_RAW);
+      else LBM_TMAK(double, lbm::CORE_GENERIC);
+    } else {
+      if (kind == lbm::CORE_PAPER) LBM_TMAK(float, lbm::CORE_PAPER);
+      else if (kind == lbm::CORE_RAW) LBM_TMAK(float, lbm::CORE_RAW);
+      else LBM_TMAK(float, lbm::CORE_GENERIC);
+    }
+#undef LBM_TMAK
   } else if (h->xpair && !fp64 && !h->fd) {
     const dim3 gp(unsigned((h->nxy / 2 + lbm::kBlock - 1) / lbm::kBlock), unsigned(nplanes), 1);
     if (h->p.model == LBM_MODEL_RM)
@@ -477,6 +500,61 @@ int launch_density(lbm_cuboid* h, const void* src, int zbeg, int nplanes, int zs
   CU(cudaGetLastError());
   if (!h->capturing) h->launches++;
   return LBM_OK;
+}
+
+// TMA kernel: tensor maps of both buffers, shared-memory opt-in, persistent grid
+typedef CUresult (*PfnEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+template <typename F>
+int driver_fn(const char* name, F* out);
+
+template <typename T>
+int tma_kernel_setup(lbm_cuboid* h, const void* fn) {
+  const int smem = int(lbm::tma_smem_bytes<T>());
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0, sms = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, lbm::kTmaThreads, smem));
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->p.device));
+  if (per_sm < 1) return fail(LBM_ECUDA, "TMA kernel cannot be resident");
+  h->tma_grid = per_sm * sms;
+  return LBM_OK;
+}
+
+int tma_setup(lbm_cuboid* h) {
+  PfnEncodeTiled enc = nullptr;
+  int rc;
+  if ((rc = driver_fn("cuTensorMapEncodeTiled", &enc))) return rc;
+  const bool fp64 = (h->p.precision == LBM_FP64);
+  const cuuint64_t e = fp64 ? 8 : 4;
+  const cuuint64_t dims[3] = {cuuint64_t(h->p.nx), cuuint64_t(h->p.ny), cuuint64_t(27) * cuuint64_t(h->nzl + 2)};
+  const cuuint64_t strides[2] = {cuuint64_t(h->p.nx) * e, cuuint64_t(h->nxy) * e};
+  // boxes: the tile (e_x = 0), the tile widened by 16 bytes on both sides (e_x
+  // = +-1: a box must start on a 16-byte boundary), 16 bytes (the x-wrap column)
+  const cuuint32_t V = cuuint32_t(16 / e);
+  const cuuint32_t boxes[3][3] = {{cuuint32_t(lbm::kTmaTx), 1, 1}, {cuuint32_t(lbm::kTmaTx) + 2 * V, 1, 1}, {V, 1, 1}};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  for (int i = 0; i < 2; ++i) {
+    CUtensorMap* maps[3] = {&h->tmaps[i].center, &h->tmaps[i].shift, &h->tmaps[i].wrap};
+    for (int w = 0; w < 3; ++w) {
+      CUresult r = enc(maps[w], fp64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, h->buf[i],
+                       dims, strides, boxes[w], estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(LBM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+    }
+  }
+  using namespace lbm;
+  const int kind = (h->p.model == LBM_MODEL_RM) ? CORE_RAW : (h->paper_rates ? CORE_PAPER : CORE_GENERIC);
+  const void* fn;
+  if (fp64)
+    fn = kind == CORE_PAPER ? (const void*)k_collide_stream_tma<double, CORE_PAPER>
+         : kind == CORE_RAW ? (const void*)k_collide_stream_tma<double, CORE_RAW>
+                            : (const void*)k_collide_stream_tma<double, CORE_GENERIC>;
+  else
+    fn = kind == CORE_PAPER ? (const void*)k_collide_stream_tma<float, CORE_PAPER>
+         : kind == CORE_RAW ? (const void*)k_collide_stream_tma<float, CORE_RAW>
+                            : (const void*)k_collide_stream_tma<float, CORE_GENERIC>;
+  return fp64 ? tma_kernel_setup<double>(h, fn) : tma_kernel_setup<float>(h, fn);
 }
 
 void drop_graphs(lbm_cuboid* h) {
@@ -1018,6 +1096,16 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   for (int i = 0; i < nbuf; ++i)
     if (cudaMemsetAsync(h->buf[i], 0, bytes, h->stream) != cudaSuccess)
       return bail(fail(LBM_ECUDA, "cudaMemsetAsync failed"));
+  {
+    // TMA-staged kernel (opt-in, LBM_TMA=1: measured slower than the LDG kernel,
+    // DESIGN §7): rows whose byte stride is a multiple of 16, 16-byte aligned
+    // buffers, at least one full tile per row; AB streaming, not FULL_FD
+    const size_t align = uintptr_t(h->buf[0]) | uintptr_t(h->buf[1]);
+    const char* tma_env = std::getenv("LBM_TMA");
+    h->tma = tma_env && std::atoi(tma_env) != 0 && !h->aa && !h->fd && (size_t(p->nx) * h->elem) % 16 == 0 &&
+             p->nx >= lbm::kTmaTx && (align % 16) == 0;
+    if (h->tma && (rc = tma_setup(h))) return bail(rc);
+  }
   if (p->check_every > 0 &&
       (cudaHostAlloc(&h->h_watch, 8 * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
        cudaEventCreateWithFlags(&h->ev_watch, cudaEventDisableTiming) != cudaSuccess))
