@@ -21,6 +21,8 @@ fields, K steps, device->host copy of rho and u, all inside the timed region.
 from __future__ import annotations
 
 import argparse
+import glob
+import hashlib
 import json
 import os
 import subprocess
@@ -37,6 +39,8 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 METRIC = "D3Q27 cuboid CM-LBM MLUPS (fp64) at 1/2/4/8 B200; achieved roofline fraction"
+# the one bounded oracle sample both CPU legs time (cpu_baseline and --impl reference)
+ORACLE_SAMPLE = (48, 48, 24)
 
 
 def parse():
@@ -59,6 +63,9 @@ def parse():
                          "exchange on the comm stream, interior launch) even on one GPU (send to self); "
                          "p2p: fused halo (the boundary-plane kernel stores into the neighbours' ghost "
                          "planes over peer memory, concurrent with the interior; on one GPU into its own)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: print this rank's plan (slab, workload, launches) and, under torchrun, "
+                         "check the max-over-ranks aggregation over a gloo process group")
     return ap.parse_args()
 
 
@@ -145,16 +152,35 @@ def measured_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(workload_name, precision):
-    """dram bytes (read + write) per launch of the collide-stream kernel from the
-    committed ncu --set full summary, if one matches this workload."""
+def kernel_source_hash():
+    """sha256 (16 hex digits) of the CUDA sources and the ABI header: the key that
+    ties a committed ncu traffic measurement to the build it was taken on."""
+    h = hashlib.sha256()
+    files = sorted(glob.glob(os.path.join(ROOT, "paper_2107_14774_b200", "csrc", "*.cu*")))
+    files.append(os.path.join(ROOT, "include", "lbm_cuboid.h"))
+    for f in files:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def ncu_traffic(workload_name, precision, kernel, nodes_per_launch):
+    """dram bytes (read + write) per launch of the collide-stream kernel from a
+    committed ncu capture (profiles/ncu_traffic.json, written by
+    scripts/ncu_traffic_update.py) of THIS build (kernel source hash), workload,
+    precision, kernel and launch size; None if no capture matches."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(path):
-        return None
+        return None, "no profiles/ncu_traffic.json"
     with open(path) as fh:
-        d = json.load(fh)
-    e = d.get(f"{workload_name}/{precision}")
-    return None if e is None else e.get("dram_bytes_per_launch")
+        entries = json.load(fh).get("entries", [])
+    src = kernel_source_hash()
+    for e in entries:
+        if (e.get("workload"), e.get("precision"), e.get("kernel"), int(e.get("nodes_per_launch", -1)),
+                e.get("source_hash")) == (workload_name, precision, kernel, int(nodes_per_launch), src):
+            return e["dram_bytes_per_launch"], e.get("source", "")
+    return None, f"no ncu capture of this build (kernel sources {src}) for this workload/kernel/launch size"
 
 
 # --------------------------------------------------------------- cpu oracle
@@ -184,7 +210,7 @@ class pinned_to_one_core:
         os.sched_setaffinity(0, self.prev)
 
 
-def oracle_mlups(w, budget_s=15.0, grid=(64, 64, 32), max_steps=None):
+def oracle_mlups(w, budget_s=15.0, grid=ORACLE_SAMPLE, max_steps=None):
     """The CPU oracle as it stands (single thread, pinned to one core), on a
     bounded sample of the workload: same physics on a smaller grid, as many
     steps as fit in budget_s."""
@@ -216,7 +242,7 @@ def run_reference(args):
     steps, warm = args.steps, args.warmup
     import oracle as O
 
-    ws = w.scaled(nx=48, ny=48, nz=24)
+    ws = w.scaled(nx=ORACLE_SAMPLE[0], ny=ORACLE_SAMPLE[1], nz=ORACLE_SAMPLE[2])
     o = O.Oracle(**ws.params())
     rho, u = synth.initial_fields(ws)
     o.init_fields(rho, u)
@@ -263,6 +289,9 @@ def run_cuda(args):
     if args.halo == "p2p":
         kw["halo"] = P.HALO_P2P
     if world > 1:
+        # NCCL's own INIT lines (rank / nranks of every communicator) for the record
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         lat = P.distributed_lattice(device=local, **kw)
     elif args.halo == "nccl":
         lat = P.Lattice(device=local, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id(), **kw)
@@ -386,14 +415,18 @@ def run_cuda(args):
     peak, peak_src = measured_peaks()
     achieved = bpn * nodes_per_launch / (kernel_ms * 1e-3) / 1e9
     prec = "fp64" if w.precision == 0 else "fp32"
-    traffic = ncu_traffic(w.name, prec)
     kname = ("k_collide_stream_raw" if w.model == synth.MODEL_RM else
              "k_collide_stream_paper" if lat.info()["paper_rate_kernel"] else "k_collide_stream")
     if args.streaming == "aa":
         kname = "k_aa (odd/even)"
+    if args.corrections == "full_fd":
+        kname = "k_collide_stream_fd" if prec == "fp64" else kname + " + k_density"
+    kfull = f"{kname}<{'double' if prec == 'fp64' else 'float'}>"
+    traffic, traffic_src = ncu_traffic(w.name, prec, kfull, nodes_per_launch)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_source": peak_src,
-            "kernel": f"{kname}<{'double' if prec == 'fp64' else 'float'}>",
+            "traffic": traffic, "traffic_source": traffic_src, "source_hash": kernel_source_hash(),
+            "peak_source": peak_src,
+            "kernel": kfull,
             "bytes_per_node": bpn, "nodes_per_launch": nodes_per_launch, "kernel_ms_mean": kernel_ms,
             "launches_timed": tk["launches"],
             "note": "achieved = 2*27*sizeof(real) B/node x nodes per launch / mean launch duration (library "
@@ -417,6 +450,7 @@ def run_cuda(args):
                               f"buffers ({lat.info()['buffer_bytes'] / 1e6:.1f} MB each) fit in L2: 512 MB L2 "
                               "flush (untimed) before every step, per-step CUDA events summed"),
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
+                       "nccl_comm": dict(zip(("nranks", "rank"), lat.comm_ranks())),
                        "halo": {0: "in-kernel wrap", 1: "nccl ghost planes", 2: "fused p2p ghost planes"}[lat.info()["halo"]],
                        "streaming": "AA in place (1 buffer)" if args.streaming == "aa" else "AB (2 buffers)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
@@ -426,9 +460,48 @@ def run_cuda(args):
         dist.destroy_process_group()
 
 
+def dry_run(args):
+    """The launch plan of this rank without a GPU (what a torchrun N-GPU run would
+    do), and, with WORLD_SIZE > 1, the max-over-ranks aggregation of per-rank
+    times over a gloo process group: rank 0 prints one JSON line."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    w = workload(args, world)
+    z0, z1 = synth.slab_range(w.nz, rank, world)
+    halo = ("in-kernel wrap" if world == 1 and args.halo == "auto" else
+            "fused p2p ghost planes" if args.halo == "p2p" else "nccl ghost planes")
+    launches_per_step = 1 if halo == "in-kernel wrap" else 2  # boundary planes + interior
+    plan = {"rank": rank, "world": world, "workload": w.name, "grid_global": [w.nx, w.ny, w.nz],
+            "slab": [z0, z1], "nodes_local": w.nx * w.ny * (z1 - z0), "halo": halo,
+            "gpu_launches_timed": launches_per_step * args.steps}
+    # a fake per-rank device time (ms) that differs between ranks; value = global nodes x K / max
+    t = 10.0 + rank
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+        x = torch.tensor([t], dtype=torch.float64)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        t = float(x.item())
+        plans = [None] * world
+        dist.all_gather_object(plans, plan)
+        dist.destroy_process_group()
+    else:
+        plans = [plan]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "scaling": "weak" if args.workload == "weak" else "strong",
+                          "max_rank_ms": t, "value": w.nodes * args.steps / (t * 1e-3) / 1e6, "plans": plans}),
+              flush=True)
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.dry_run:
+        dry_run(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_cuda(args)

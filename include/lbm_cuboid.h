@@ -262,6 +262,12 @@ int lbm_cuboid_info(const lbm_cuboid_t *h, int64_t out[8]);
 /* cudaStream_t of the compute stream (for event timing by the caller). */
 void *lbm_cuboid_stream(const lbm_cuboid_t *h);
 
+/* The handle's NCCL communicator (ghost-plane exchange with LBM_HALO_AUTO at
+ * world > 1, or LBM_HALO_NCCL): out[0] = ncclCommCount, out[1] = this rank in
+ * it (ncclCommUserRank); both -1 when the handle has no communicator (single
+ * GPU with in-kernel wrap, or the fused P2P halo).  Host-only query. */
+int lbm_cuboid_comm_ranks(const lbm_cuboid_t *h, int32_t out[2]);
+
 /* Per-launch timing of the collide-stream kernel: while enabled, every launch
  * is bracketed by a CUDA event pair on the compute stream (at most 65536
  * launches are recorded).  lbm_cuboid_timing() synchronises and clears the
@@ -270,6 +276,21 @@ void *lbm_cuboid_stream(const lbm_cuboid_t *h);
  * out[2] = node updates they performed. */
 int lbm_cuboid_timing(lbm_cuboid_t *h, int enable);
 int lbm_cuboid_timing_read(lbm_cuboid_t *h, double out[3]);
+
+/* Trace of the step structure (SURVEY §5 tracing; nsys is not available on this
+ * pool): while enabled, every collide-stream / density launch and every NCCL
+ * halo exchange is bracketed by a CUDA event pair on the stream it is enqueued
+ * on (compute stream 0, halo/comm stream 1), so the overlap of the boundary
+ * planes, the halo and the interior can be read back (CUDA graphs are not used
+ * while tracing).  lbm_cuboid_trace() synchronises, clears the record and
+ * starts it (enable != 0) or stops it.  lbm_cuboid_trace_read() synchronises
+ * and writes min(max_rows, recorded) rows of 6 doubles into out:
+ * {kind (0 collide-stream launch, 1 boundary-plane launch, 2 NCCL halo
+ * exchange, 3 density pass), stream (0 compute, 1 halo), first plane, planes,
+ * start ms, end ms} (times from the enable call's event on the compute stream);
+ * *rows = number recorded (at most 65536). */
+int lbm_cuboid_trace(lbm_cuboid_t *h, int enable);
+int lbm_cuboid_trace_read(lbm_cuboid_t *h, double *out, int32_t max_rows, int32_t *rows);
 
 /* Release library state (streams, events, NCCL comm, library-owned buffers).
  * Caller-owned buffers are untouched.  NULL is accepted. */

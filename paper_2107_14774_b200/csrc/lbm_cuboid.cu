@@ -137,11 +137,42 @@ struct lbm_cuboid {
   bool capturing = false;
   // optional per-launch timing of the collide-stream kernel (lbm_cuboid_timing)
   bool timing = false;
+  // optional trace of the step structure (lbm_cuboid_trace): an event pair per
+  // launch / halo exchange on the stream it runs on, relative to trace_base
+  bool tracing = false;
+  cudaEvent_t trace_base = nullptr;
+  struct TraceRec {
+    int kind, stream, zbeg, nplanes;
+    cudaEvent_t a, b;
+  };
+  std::vector<TraceRec> trace;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_t;
   std::vector<int64_t> ev_t_nodes;
 };
 
 namespace {
+
+// trace record kinds (lbm_cuboid_trace_read)
+enum { TR_COLLIDE = 0, TR_BOUNDARY = 1, TR_NCCL = 2, TR_DENSITY = 3 };
+constexpr size_t kMaxTrace = 1 << 16;
+
+// event pair around work enqueued on stream s (no-op unless tracing)
+struct TraceScope {
+  lbm_cuboid* h;
+  cudaStream_t s;
+  int idx = -1;
+  TraceScope(lbm_cuboid* hh, cudaStream_t ss, int kind, int zbeg, int nplanes) : h(hh), s(ss) {
+    if (!h->tracing || h->capturing || h->trace.size() >= kMaxTrace) return;
+    lbm_cuboid::TraceRec r{kind, s == h->stream ? 0 : 1, zbeg, nplanes, nullptr, nullptr};
+    if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
+    cudaEventRecord(r.a, s);
+    h->trace.push_back(r);
+    idx = int(h->trace.size()) - 1;
+  }
+  ~TraceScope() {
+    if (idx >= 0) cudaEventRecord(h->trace[idx].b, s);
+  }
+};
 
 int set_device(const lbm_cuboid* h) {
   CU(cudaSetDevice(h->p.device));
@@ -320,6 +351,8 @@ lbm::P2PArgs<T> p2p_args(const lbm_cuboid* h, int which, uint32_t epoch) {
 int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, int zstride, cudaStream_t s,
               int p2p_which = -1, uint32_t p2p_epoch = 0, bool allow_timing = true) {
   if (nplanes <= 0) return LBM_OK;
+  // ghost-plane mode: the boundary-plane launch starts at plane 0, the interior at 1
+  TraceScope trace_scope(h, s, (h->ghost && zbeg == 0) ? TR_BOUNDARY : TR_COLLIDE, zbeg, nplanes);
   dim3 g = grid_for(h, nplanes);
   const bool fp64 = (h->p.precision == LBM_FP64);
   const bool timed = allow_timing && h->timing && h->ev_t.size() < kMaxTimedLaunches;
@@ -492,6 +525,7 @@ int aa_mode(const lbm_cuboid* h) { return h->aa ? (h->cur == 0 ? 1 : 2) : 0; }
 // FULL_FD density pass over planes zbeg + i*zstride of the local slab
 int launch_density(lbm_cuboid* h, const void* src, int zbeg, int nplanes, int zstride, cudaStream_t s) {
   if (nplanes <= 0) return LBM_OK;
+  TraceScope trace_scope(h, s, TR_DENSITY, zbeg, nplanes);
   dim3 g = grid_for(h, nplanes);
   if (h->p.precision == LBM_FP64)
     lbm::k_density<double><<<g, lbm::kBlock, 0, s>>>((const double*)src, h->d_rho, h->c, zbeg, zstride);
@@ -572,7 +606,7 @@ bool use_persistent(const lbm_cuboid* h) {
 }
 
 bool use_graphs(const lbm_cuboid* h) {
-  if (h->ghost || h->timing || h->p.graphs == 1 || h->p.graphs == 3) return false;
+  if (h->ghost || h->timing || h->tracing || h->p.graphs == 1 || h->p.graphs == 3) return false;
   return h->p.graphs == 2 || h->nxy * h->nzl < kGraphMaxNodes;
 }
 
@@ -695,6 +729,7 @@ int exchange(lbm_cuboid* h, int which) {
   CU(cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
   const HaloPlan hp = make_plan(&h->p);
   const ncclDataType_t dt = (h->p.precision == LBM_FP64) ? ncclDouble : ncclFloat;
+  TraceScope trace_scope(h, h->comm_stream, TR_NCCL, 0, 2);
   char* b = (char*)h->buf[which];
   const size_t e = h->elem, cnt = size_t(hp.count);
   // NCCL matches the sends and recvs between one pair of ranks in issue order;
@@ -1457,6 +1492,18 @@ int lbm_cuboid_info(const lbm_cuboid_t* h, int64_t out[8]) {
 
 void* lbm_cuboid_stream(const lbm_cuboid_t* h) { return h ? (void*)h->stream : nullptr; }
 
+int lbm_cuboid_comm_ranks(const lbm_cuboid_t* h, int32_t out[2]) {
+  if (!h || !out) return fail(LBM_EINVAL, "NULL argument");
+  out[0] = out[1] = -1;
+  if (!h->comm) return LBM_OK;
+  int n = 0, r = 0;
+  NC(ncclCommCount(h->comm, &n));
+  NC(ncclCommUserRank(h->comm, &r));
+  out[0] = n;
+  out[1] = r;
+  return LBM_OK;
+}
+
 static void clear_timing(lbm_cuboid_t* h) {
   for (auto& e : h->ev_t) {
     cudaEventDestroy(e.first);
@@ -1492,6 +1539,58 @@ int lbm_cuboid_timing_read(lbm_cuboid_t* h, double out[3]) {
   out[0] = double(h->ev_t.size());
   out[1] = ms;
   out[2] = double(nodes);
+  return LBM_OK;
+}
+
+static void clear_trace(lbm_cuboid_t* h) {
+  for (auto& r : h->trace) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  h->trace.clear();
+  if (h->trace_base) {
+    cudaEventDestroy(h->trace_base);
+    h->trace_base = nullptr;
+  }
+}
+
+int lbm_cuboid_trace(lbm_cuboid_t* h, int enable) {
+  if (!h) return fail(LBM_EINVAL, "NULL handle");
+  int rc = set_device(h);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(h->stream));
+  if (h->comm_stream) CU(cudaStreamSynchronize(h->comm_stream));
+  clear_trace(h);
+  h->tracing = (enable != 0);
+  if (h->tracing) {
+    drop_graphs(h);  // launches inside replayed graphs carry no events
+    CU(cudaEventCreate(&h->trace_base));
+    CU(cudaEventRecord(h->trace_base, h->stream));
+  }
+  return LBM_OK;
+}
+
+int lbm_cuboid_trace_read(lbm_cuboid_t* h, double* out, int32_t max_rows, int32_t* rows) {
+  if (!h || !rows || (max_rows > 0 && !out)) return fail(LBM_EINVAL, "NULL argument");
+  int rc = set_device(h);
+  if (rc) return rc;
+  CU(cudaStreamSynchronize(h->stream));
+  if (h->comm_stream) CU(cudaStreamSynchronize(h->comm_stream));
+  *rows = int32_t(h->trace.size());
+  const int n = std::min<int>(max_rows, int(h->trace.size()));
+  for (int i = 0; i < n; ++i) {
+    const auto& r = h->trace[i];
+    float ta = 0.f, tb = 0.f;
+    CU(cudaEventElapsedTime(&ta, h->trace_base, r.a));
+    CU(cudaEventElapsedTime(&tb, h->trace_base, r.b));
+    double* o = out + 6 * i;
+    o[0] = r.kind;
+    o[1] = r.stream;
+    o[2] = r.zbeg;
+    o[3] = r.nplanes;
+    o[4] = ta;
+    o[5] = tb;
+  }
   return LBM_OK;
 }
 
@@ -1643,6 +1742,7 @@ int lbm_cuboid_destroy(lbm_cuboid_t* h) {
   if (h->d_rho) cudaFree(h->d_rho);
   if (h->ev_rho) cudaEventDestroy(h->ev_rho);
   clear_timing(h);
+  clear_trace(h);
   drop_graphs(h);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;

@@ -35,7 +35,8 @@ EXPORTS = ["lbm_cuboid_default_params", "lbm_cuboid_buffer_bytes", "lbm_cuboid_h
            "lbm_cuboid_step", "lbm_cuboid_sync", "lbm_cuboid_get_macroscopic",
            "lbm_cuboid_get_macroscopic_device", "lbm_cuboid_get_populations",
            "lbm_cuboid_get_populations_planes", "lbm_cuboid_set_populations", "lbm_cuboid_check", "lbm_cuboid_set_force",
-           "lbm_cuboid_info", "lbm_cuboid_stream", "lbm_cuboid_timing", "lbm_cuboid_timing_read",
+           "lbm_cuboid_info", "lbm_cuboid_stream", "lbm_cuboid_comm_ranks", "lbm_cuboid_timing", "lbm_cuboid_timing_read",
+           "lbm_cuboid_trace", "lbm_cuboid_trace_read",
            "lbm_cuboid_destroy", "lbm_cuboid_last_error"]
 
 
@@ -94,6 +95,12 @@ def load():
     L.lbm_cuboid_info.argtypes = [_VP, ctypes.POINTER(ctypes.c_int64)]
     L.lbm_cuboid_stream.argtypes = [_VP]
     L.lbm_cuboid_stream.restype = _VP
+    L.lbm_cuboid_comm_ranks.argtypes = [_VP, ctypes.POINTER(ctypes.c_int32)]
+    L.lbm_cuboid_comm_ranks.restype = ctypes.c_int
+    L.lbm_cuboid_trace.argtypes = [_VP, ctypes.c_int]
+    L.lbm_cuboid_trace.restype = ctypes.c_int
+    L.lbm_cuboid_trace_read.argtypes = [_VP, _D, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
+    L.lbm_cuboid_trace_read.restype = ctypes.c_int
     L.lbm_cuboid_timing.argtypes = [_VP, ctypes.c_int]
     L.lbm_cuboid_timing_read.argtypes = [_VP, _D]
     L.lbm_cuboid_destroy.argtypes = [_VP]
@@ -300,6 +307,26 @@ class Lattice:
         keys = ["launches", "collide_stream_launches", "steps", "bytes_per_node_update",
                 "local_nodes", "buffer_bytes", "halo", "paper_rate_kernel"]
         return dict(zip(keys, list(a)))
+
+    def trace(self, enable: bool):
+        """Start (and clear) / stop the event trace of the step structure."""
+        _check(load().lbm_cuboid_trace(self._h, 1 if enable else 0))
+
+    def trace_read(self):
+        """Recorded launches: list of dicts kind/stream/zbeg/nplanes/t0_ms/t1_ms."""
+        n = ctypes.c_int32(0)
+        _check(load().lbm_cuboid_trace_read(self._h, None, 0, ctypes.byref(n)))
+        a = np.zeros((max(n.value, 1), 6))
+        _check(load().lbm_cuboid_trace_read(self._h, a.ctypes.data_as(_D), n.value, ctypes.byref(n)))
+        kinds = {0: "collide", 1: "boundary", 2: "nccl_halo", 3: "density"}
+        return [{"kind": kinds[int(r[0])], "stream": "compute" if r[1] == 0 else "halo", "zbeg": int(r[2]),
+                 "nplanes": int(r[3]), "t0_ms": float(r[4]), "t1_ms": float(r[5])} for r in a[:n.value]]
+
+    def comm_ranks(self):
+        """(nranks, rank) of the library's NCCL communicator, (-1, -1) without one."""
+        a = (ctypes.c_int32 * 2)()
+        _check(load().lbm_cuboid_comm_ranks(self._h, a))
+        return int(a[0]), int(a[1])
 
     def p2p_export(self) -> bytes:
         """This slab's LBM_HALO_P2P descriptor (IPC handles + addresses), for its neighbours."""

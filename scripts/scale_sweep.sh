@@ -1,16 +1,20 @@
 # Weak and strong scaling on the GPUs of one box, both halo modes (run when more
 # than one GPU is available):  bash scripts/scale_sweep.sh [max_gpus] > scale.jsonl
+# DRY_RUN=1: no GPU -- every bench.py call gets --dry-run (plan + gloo aggregation
+# check), so the launch logic of the sweep runs on a CPU (tests/test_bench_dryrun.py).
 cd ${GRAFT_REPO_ROOT:-$(dirname "$0")/..}
 MAX=${1:-$(nvidia-smi -L | wc -l)}
-PORT=29600
+PORT=${PORT:-29600}
+DRY=""
+[ -n "$DRY_RUN" ] && DRY="--dry-run"
 run() {  # n, extra bench args...
   local n=$1; shift
   PORT=$((PORT + 1))
   if [ "$n" = 1 ]; then
-    timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-e2e --no-cpu-baseline "$@" | tail -1
+    timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 --no-e2e --no-cpu-baseline $DRY "$@" | tail -1
   else
     timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node "$n" --master-addr 127.0.0.1 \
-      --master-port $PORT bench.py --gpus "$n" --steps 20 --warmup 5 --no-e2e --no-cpu-baseline "$@" | tail -1
+      --master-port $PORT bench.py --gpus "$n" --steps 20 --warmup 5 --no-e2e --no-cpu-baseline $DRY "$@" 2>/dev/null | tail -1
   fi
 }
 for n in 1 2 4 8; do
