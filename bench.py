@@ -56,7 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--nz-per-gpu", type=int, default=None, help="override the per-GPU slab depth")
-    ap.add_argument("--corrections", choices=["full_local", "low_mach", "off", "full_fd"], default="full_local")
+    ap.add_argument("--corrections", choices=["full_local", "low_mach", "off", "full_fd", "full_fd_lag"],
+                    default="full_local")
     ap.add_argument("--model", choices=["cm", "rm"], default="cm")
     ap.add_argument("--halo", choices=["auto", "nccl", "p2p"], default="auto",
                     help="nccl: force the multi-GPU step structure (boundary launch, NCCL ghost-plane "
@@ -74,7 +75,7 @@ def workload(args, world):
     if args.precision == "fp32":
         w = w.scaled(precision=synth.PREC_FP32)
     corr = {"full_local": synth.CORR_FULL_LOCAL, "low_mach": synth.CORR_LOW_MACH, "off": synth.CORR_OFF,
-            "full_fd": synth.CORR_FULL_FD}[args.corrections]
+            "full_fd": synth.CORR_FULL_FD, "full_fd_lag": synth.CORR_FULL_FD_LAG}[args.corrections]
     w = w.scaled(corrections=corr, model=synth.MODEL_RM if args.model == "rm" else synth.MODEL_CM)
     nzl = args.nz_per_gpu or w.nz
     if args.workload == "weak":

@@ -72,9 +72,15 @@ typedef enum {
   LBM_CORR_FULL_LOCAL = 0, /* theta with the 3u^2 aliasing terms; local strain rates; lambda = e_rho = 0 */
   LBM_CORR_LOW_MACH = 1,   /* 3u^2 terms dropped (in theta and in the strain-rate solve) */
   LBM_CORR_OFF = 2,        /* no corrections (ablation) */
-  LBM_CORR_FULL_FD = 3     /* FULL_LOCAL plus the density-gradient terms lambda and e_rho,
-                              with the isotropic lattice gradient of a same-time density field:
-                              one extra density pass per step (+216 B/node of HBM traffic) */
+  LBM_CORR_FULL_FD = 3,    /* FULL_LOCAL plus the density-gradient terms lambda and e_rho,
+                              with the isotropic lattice gradient of a same-time density field (P:L494,
+                              DESIGN reading R16): the density of the pulled populations of every
+                              neighbour (fused 2.5D kernel for fp64, density pass + collide for fp32) */
+  LBM_CORR_FULL_FD_LAG = 4 /* the same terms with the gradient of the STORED state's density, one time
+                              level earlier (reading R16b: the paper does not fix the time level of
+                              P:L1181); the collision writes each node's density into a second field
+                              that the next step's gradient reads: 2*27*sizeof(real) + 16 B/node;
+                              pinned by the same moving-frame acoustic attenuation as FULL_FD */
 } lbm_corr;
 
 typedef enum {
@@ -94,7 +100,7 @@ typedef enum {
   LBM_STREAM_AA = 1  /* one buffer updated in place, alternating an "odd" step (pull from reversed
                         slots, collide, push) and an "even" step (collide in place, store reversed):
                         half the memory, same 2*27*sizeof(real) bytes per node update; single GPU,
-                        not with LBM_CORR_FULL_FD */
+                        not with LBM_CORR_FULL_FD / LBM_CORR_FULL_FD_LAG */
 } lbm_streaming;
 
 typedef enum {

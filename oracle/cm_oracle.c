@@ -33,7 +33,8 @@
  * R6 (a wall wins over periodicity), R7 (free-slip = halfway specular
  * reflection), R8 (init f~ = f^eq(rho0, u0 + F/(2 rho0))), R16 (FULL_FD: the
  * isotropic lattice gradient of the same-time density, mirror-image neighbours
- * across walls).
+ * across walls), R16b (FULL_FD_LAG: the same gradient of the stored state's
+ * density, one time level earlier), R17 (singular strain-rate system).
  *
  * Parity pins: tests/test_oracle_*.py (closed forms, paper-printed appendices
  * and Eq. 69, conservation, SRT limit, order of the corrections (slope 3 on the
@@ -76,7 +77,9 @@ static const int MIDX[3][3][3] = {
 #define midx(m, n, p) MIDX[m][n][p]
 
 enum { BC_PERIODIC = 0, BC_BOUNCE_BACK = 1, BC_MOVING_WALL = 2, BC_FREE_SLIP = 3 };
-enum { CORR_FULL_LOCAL = 0, CORR_LOW_MACH = 1, CORR_OFF = 2, CORR_FULL_FD = 3 };
+enum { CORR_FULL_LOCAL = 0, CORR_LOW_MACH = 1, CORR_OFF = 2, CORR_FULL_FD = 3, CORR_FULL_FD_LAG = 4 };
+/* the density-gradient (lambda, e_rho) modes: same-time density (R16) or the stored state's (R16b) */
+#define FD_MODE(c) ((c) == CORR_FULL_FD || (c) == CORR_FULL_FD_LAG)
 
 typedef struct {
   int32_t nx, ny, nz;
@@ -340,7 +343,7 @@ void oracle_collide_g(const oracle_ctx *c, const double *f, const double *grad_r
    * with the coefficients of P:L1171-1180 and local strain rates of P:L1183-1203. */
   double k2s_eq = 3.0 * cs2 * rho, k2d1_eq = 0.0, k2d2_eq = 0.0;
   if (p->corrections != CORR_OFF) {
-    const double g = (p->corrections == CORR_FULL_LOCAL || p->corrections == CORR_FULL_FD) ? 1.0 : 0.0; /* aliasing (3u^2) terms */
+    const double g = (p->corrections == CORR_FULL_LOCAL || FD_MODE(p->corrections)) ? 1.0 : 0.0; /* aliasing (3u^2) terms */
     const double an = 1.0 / wn - 0.5, ab = 1.0 / wx - 0.5;
     double th_sx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * an;
     double th_bx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * ab;
@@ -351,7 +354,7 @@ void oracle_collide_g(const oracle_ctx *c, const double *f, const double *grad_r
     /* density-gradient terms: only in CORR_FULL_FD
      * (reading R1: FULL_LOCAL and LOW_MACH set lambda = e_rho = 0) */
     double gx = 0.0, gy = 0.0, gz = 0.0;
-    if (p->corrections == CORR_FULL_FD && grad_rho) {
+    if (FD_MODE(p->corrections) && grad_rho) {
       gx = grad_rho[0];
       gy = grad_rho[1];
       gz = grad_rho[2];
@@ -476,7 +479,7 @@ void oracle_collide_raw_g(const oracle_ctx *c, const double *f, const double *gr
   double p2s = PH(2, 0, 0) + PH(0, 2, 0) + PH(0, 0, 2), p2d1 = PH(2, 0, 0) - PH(0, 2, 0),
          p2d2 = PH(2, 0, 0) - PH(0, 0, 2);
   if (p->corrections != CORR_OFF) {
-    const double g = (p->corrections == CORR_FULL_LOCAL || p->corrections == CORR_FULL_FD) ? 1.0 : 0.0;
+    const double g = (p->corrections == CORR_FULL_LOCAL || FD_MODE(p->corrections)) ? 1.0 : 0.0;
     const double an = 1.0 / wn - 0.5, ab = 1.0 / wx - 0.5;
     double th_sx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * an;
     double th_bx = -rho * (g * 3.0 * ux * ux + 3.0 * cs2 - 1.0) * ab;
@@ -485,7 +488,7 @@ void oracle_collide_raw_g(const oracle_ctx *c, const double *f, const double *gr
     double th_sz = -rho * (g * 3.0 * uz * uz + 3.0 * cs2 - s2) * an;
     double th_bz = -rho * (g * 3.0 * uz * uz + 3.0 * cs2 - s2) * ab;
     double gx = 0.0, gy = 0.0, gz = 0.0;
-    if (p->corrections == CORR_FULL_FD && grad_rho) {
+    if (FD_MODE(p->corrections) && grad_rho) {
       gx = grad_rho[0];
       gy = grad_rho[1];
       gz = grad_rho[2];
@@ -665,12 +668,17 @@ void oracle_density_gradient(const oracle_ctx *c, const double *rho, int x, int 
 
 /* One time step on the whole grid: fdst = collide(pull(fsrc)).  With
  * CORR_FULL_FD the step is done in two passes: pull every node and form the
- * same-time density field, then collide with its isotropic gradient. */
+ * same-time density field (reading R16), then collide with its isotropic
+ * gradient.  With CORR_FULL_FD_LAG (reading R16b) the density field is that of
+ * the stored state, rho(x, t) = sum_q f~_q(x, t) at every node (the density of
+ * the previous collision: the collision conserves mass), one time level behind
+ * the populations it corrects. */
 void oracle_step(const oracle_ctx *c, const double *fsrc, double *fdst) {
   const oracle_params *p = &c->p;
   const int64_t nn = (int64_t)p->nx * p->ny * p->nz;
   double f[NQ], ft[NQ], g[3];
-  const int fd = (p->corrections == CORR_FULL_FD);
+  const int fd = FD_MODE(p->corrections);
+  const int lag = (p->corrections == CORR_FULL_FD_LAG);
   double *rho = NULL;
   if (fd) {
     rho = (double *)malloc(sizeof(double) * nn);
@@ -678,7 +686,8 @@ void oracle_step(const oracle_ctx *c, const double *fsrc, double *fdst) {
       for (int y = 0; y < p->ny; ++y)
         for (int x = 0; x < p->nx; ++x) {
           double r0 = 0.0;
-          for (int q = 0; q < NQ; ++q) r0 += pull(c, fsrc, x, y, z, q);
+          for (int q = 0; q < NQ; ++q)
+            r0 += lag ? fsrc[(int64_t)q * nn + nid(p, x, y, z)] : pull(c, fsrc, x, y, z, q);
           rho[nid(p, x, y, z)] = r0;
         }
   }

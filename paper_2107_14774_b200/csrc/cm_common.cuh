@@ -60,6 +60,7 @@ struct Consts {
   unsigned int* sing_flag;    // set to 1 when a node's strain-rate system is singular (reading R17)
   double sing_thr;            // 1e-12 cs2: threshold of the singular predicate on C/rho
   double* aa_lid_rho;         // AA with the moving lid: rho of the lid-row nodes [z][x] (see k_aa)
+  double* rf_out;             // FULL_FD_LAG: density field the collision writes (the next step's gradient)
 };
 
 // Singular strain-rate system (reading R17): the closed-form

@@ -124,26 +124,27 @@ __device__ __forceinline__ void collide_stream_ab(const T* __restrict__ src, T* 
   double gxr = 0.0, gyr = 0.0, gzr = 0.0;
   if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
   gather<T>(src, c, x, y, z, f);
-  StoreOwn<T> st{dst, dst + (long long)(z + 1) * c.plane + idx, c.nxy, &c};
+  StoreOwn<T> st{dst, dst + (long long)(z + 1) * c.plane + idx, c.nxy, &c,
+                 c.rf_out ? c.rf_out + (long long)(z + 1) * c.nxy + idx : nullptr};
   run_core<KIND, FD>(c, f, gxr, gyr, gzr, st);
 }
 
 template <typename T, bool FD>
-__global__ void LBM_CS_BOUNDS k_collide_stream(const T* __restrict__ src, T* __restrict__ dst,
+__global__ void LBM_CS_BOUNDS_FD(FD) k_collide_stream(const T* __restrict__ src, T* __restrict__ dst,
                                                const double* __restrict__ rf, const __grid_constant__ Consts c,
                                                int zbeg, int zstride) {
   collide_stream_ab<T, CORE_GENERIC, FD>(src, dst, rf, c, zbeg, zstride);
 }
 
 template <typename T, bool FD>
-__global__ void LBM_CS_BOUNDS k_collide_stream_paper(const T* __restrict__ src, T* __restrict__ dst,
+__global__ void LBM_CS_BOUNDS_FD(FD) k_collide_stream_paper(const T* __restrict__ src, T* __restrict__ dst,
                                                      const double* __restrict__ rf, const __grid_constant__ Consts c,
                                                      int zbeg, int zstride) {
   collide_stream_ab<T, CORE_PAPER, FD>(src, dst, rf, c, zbeg, zstride);
 }
 
 template <typename T, bool FD>
-__global__ void LBM_CS_BOUNDS k_collide_stream_raw(const T* __restrict__ src, T* __restrict__ dst,
+__global__ void LBM_CS_BOUNDS_FD(FD) k_collide_stream_raw(const T* __restrict__ src, T* __restrict__ dst,
                                                    const double* __restrict__ rf, const __grid_constant__ Consts c,
                                                    int zbeg, int zstride) {
   collide_stream_ab<T, CORE_RAW, FD>(src, dst, rf, c, zbeg, zstride);
@@ -330,6 +331,8 @@ struct P2PArgs {
   unsigned int* flag_up; // my slot in the up neighbour's flag words (nullptr: none)
   unsigned int* flag_dn; // my slot in the down neighbour's flag words
   unsigned int epoch;    // value published when every CTA has stored
+  double* rho_up;        // FULL_FD_LAG: up / down neighbour's density field of this time level
+  double* rho_dn;        // (nullptr: none)
 };
 
 // Own-node store plus the peer copy of the outgoing directions:
@@ -346,11 +349,23 @@ struct StoreHalo {
   T* rdn;  // down neighbour's ghost plane at this node, or nullptr
   T* up_base;
   T* dn_base;
+  double* rho_own = nullptr;  // FULL_FD_LAG: own density field at this node (sum of the stored
+  double* rho_up = nullptr;   // values in q order, as StoreOwn) and the neighbours' density
+  double* rho_dn = nullptr;   // ghost planes at this node
+  double acc = 0.0;
   __device__ __forceinline__ void begin(double) {}
-  __device__ __forceinline__ void operator()(int q, double v) const {
+  __device__ __forceinline__ void operator()(int q, double v) {
     stcs<T>(LBM_CHECK_ST(base, out + q * nxy, *c), v);
     if (q >= 18 && rup) stcs<T>(LBM_CHECK_ST(up_base, rup + q * nxy, *c), v);
     if (q < 9 && rdn) stcs<T>(LBM_CHECK_ST(dn_base, rdn + q * nxy, *c), v);
+    if (rho_own) {
+      acc += (double)(T)v;
+      if (q == 26) {
+        *rho_own = acc;
+        if (rho_up) *rho_up = acc;
+        if (rho_dn) *rho_dn = acc;
+      }
+    }
   }
 };
 
@@ -396,7 +411,10 @@ __global__ void LBM_CS_BOUNDS k_collide_stream_p2p(const T* __restrict__ src, T*
                     (z == c.nzl - 1 && a.up) ? a.up + idx : nullptr,
                     (z == 0 && a.dn) ? a.dn + (long long)(c.nzl + 1) * c.plane + idx : nullptr,
                     a.up,
-                    a.dn};
+                    a.dn,
+                    c.rf_out ? c.rf_out + (long long)(z + 1) * c.nxy + idx : nullptr,
+                    (c.rf_out && z == c.nzl - 1 && a.rho_up) ? a.rho_up + idx : nullptr,                         // ghost p = 0
+                    (c.rf_out && z == 0 && a.rho_dn) ? a.rho_dn + (long long)(c.nzl + 1) * c.nxy + idx : nullptr};
     run_core<KIND, FD>(c, f, gxr, gyr, gzr, st);
   }
   p2p_signal(a);
@@ -435,8 +453,8 @@ __global__ void __launch_bounds__(kBlock) k_density_p2p(const T* __restrict__ sr
 // the outgoing directions of the two boundary planes of `src` into the
 // neighbours' ghost planes (blockIdx.y = 0: down, 1: up), then signal.
 template <typename T>
-__global__ void __launch_bounds__(kBlock) k_halo_push(const T* __restrict__ src, const __grid_constant__ Consts c,
-                                                      const P2PArgs<T> a) {
+__global__ void __launch_bounds__(kBlock) k_halo_push(const T* __restrict__ src, const double* __restrict__ rsrc,
+                                                      const __grid_constant__ Consts c, const P2PArgs<T> a) {
   const long long e = (long long)blockIdx.x * kBlock + threadIdx.x;
   if (e < 9LL * c.nxy) {
     if (blockIdx.y == 0 && a.dn)  // bottom plane p = 1, q 0..8 -> ghost p = nz_l + 1
@@ -444,7 +462,26 @@ __global__ void __launch_bounds__(kBlock) k_halo_push(const T* __restrict__ src,
     if (blockIdx.y == 1 && a.up)  // top plane p = nz_l, q 18..26 -> ghost p = 0
       a.up[18LL * c.nxy + e] = src[(long long)c.nzl * c.plane + 18LL * c.nxy + e];
   }
+  if (rsrc && e < c.nxy) {  // FULL_FD_LAG: the boundary planes' densities into the neighbours' ghost planes
+    if (blockIdx.y == 0 && a.rho_dn) a.rho_dn[(long long)(c.nzl + 1) * c.nxy + e] = rsrc[c.nxy + e];
+    if (blockIdx.y == 1 && a.rho_up) a.rho_up[e] = rsrc[(long long)c.nzl * c.nxy + e];
+  }
   p2p_signal(a);
+}
+
+// FULL_FD_LAG after init_fields / set_populations: the density field of the
+// stored state, rho = sum_q f~_q of each node of the planes zbeg + blockIdx.y
+template <typename T>
+__global__ void __launch_bounds__(kBlock) k_stored_rho(const T* __restrict__ src, double* __restrict__ rf,
+                                                       const __grid_constant__ Consts c, int zbeg) {
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int z = zbeg + blockIdx.y;
+  const T* p = src + (long long)(z + 1) * c.plane + idx;
+  double r0 = 0.0;  // q order, as StoreOwn forms it
+#pragma unroll
+  for (int q = 0; q < 27; ++q) r0 += ldg(p + q * c.nxy);
+  rf[(long long)(z + 1) * c.nxy + idx] = r0;
 }
 
 // ------------------------------------ persistent multi-step kernel (small lattices)

@@ -183,6 +183,13 @@ __device__ __forceinline__ void collide_generic(const Consts& c, double (&f)[27]
 #else
 #define LBM_CS_BOUNDS __launch_bounds__(kBlock)
 #endif
+// collide-stream kernels with the density-gradient terms (FULL_FD two-pass and
+// FULL_FD_LAG): ask for 6 resident 128-thread CTAs (<= 80 registers; 112 without
+// the bound cost ~7 % at 512^3)
+#ifndef LBM_FD_CS_MINB
+#define LBM_FD_CS_MINB 6
+#endif
+#define LBM_CS_BOUNDS_FD(FD) __launch_bounds__(kBlock, (FD) ? LBM_FD_CS_MINB : LBM_MINB)
 
 // Generic rates (any omega_1, omega_high): all 27 central moments.
 template <bool FD, class St>

@@ -187,13 +187,15 @@ __device__ __forceinline__ void gather(const T* src, const Consts& c, int x, int
 // the population-buffer plane structure: rf[(z_local + 1) * nxy + y * nx + x].
 // rho_at(i, j, k) = density at offset (i-1, j-1, k-1) from the node (never
 // called for a neighbour across a wall); identical arithmetic for every source.
-template <class RhoAt>
+// NOWALL: the caller knows no face of the node is a wall (no mirror images)
+template <class RhoAt, bool NOWALL = false>
 __device__ __forceinline__ void density_gradient_g(const Consts& c, int x, int y, int z, RhoAt rho_at, double& gx,
                                                    double& gy, double& gz) {
   auto is_wall = [](int fk) { return fk >= FK_BOUNCE && fk <= FK_SLIP; };
-  const bool cx[3] = {x == 0 && is_wall(c.face[0]), false, x == c.nx - 1 && is_wall(c.face[1])};
-  const bool cy[3] = {y == 0 && is_wall(c.face[2]), false, y == c.ny - 1 && is_wall(c.face[3])};
-  const bool cz[3] = {z == 0 && is_wall(c.face[4]), false, z == c.nzl - 1 && is_wall(c.face[5])};
+  const bool cx[3] = {!NOWALL && x == 0 && is_wall(c.face[0]), false, !NOWALL && x == c.nx - 1 && is_wall(c.face[1])};
+  const bool cy[3] = {!NOWALL && y == 0 && is_wall(c.face[2]), false, !NOWALL && y == c.ny - 1 && is_wall(c.face[3])};
+  const bool cz[3] = {!NOWALL && z == 0 && is_wall(c.face[4]), false,
+                      !NOWALL && z == c.nzl - 1 && is_wall(c.face[5])};
   double sx = 0.0, sy = 0.0, sz = 0.0;
 #pragma unroll
   for (int k = 0; k < 3; ++k)
@@ -217,6 +219,16 @@ __device__ __forceinline__ void density_gradient_g(const Consts& c, int x, int y
 __device__ __forceinline__ void density_gradient(const double* __restrict__ rf, const Consts& c, int x, int y,
                                                  int z, double& gx, double& gy, double& gz) {
   const int nx = c.nx;
+  // warp-uniform interior: no lane wraps a periodic face or touches a wall, so
+  // the 26 neighbours are the node's address plus warp-uniform offsets
+  const bool inner = x > 0 && x < nx - 1 && y > 0 && y < c.ny - 1 && !(z == 0 && c.face[4] == FK_WRAP) &&
+                     !(z == c.nzl - 1 && c.face[5] == FK_WRAP) && !wall_adjacent(c, x, y, z);
+  if (__all_sync(__activemask(), inner)) {
+    const double* b = rf + (long long)(z + 1) * c.nxy + (y * nx + x);
+    auto at = [&](int i, int j, int k) { return __ldg(b + ((long long)(k - 1) * c.nxy + ((j - 1) * nx + (i - 1)))); };
+    density_gradient_g<decltype(at), true>(c, x, y, z, at, gx, gy, gz);
+    return;
+  }
   const int xs[3] = {(x == 0) ? nx - 1 : x - 1, x, (x == nx - 1) ? 0 : x + 1};
   const int ys[3] = {((y == 0) ? c.ny - 1 : y - 1) * nx, y * nx, ((y == c.ny - 1) ? 0 : y + 1) * nx};
   int zm = z - 1, zp = z + 1;
@@ -239,9 +251,18 @@ struct StoreOwn {
   T* out;
   int nxy;
   const Consts* c;
+  // FULL_FD_LAG: the node's density for the next step's gradient, formed as the
+  // sum of the STORED values in q order (what k_stored_rho forms after a
+  // set_populations, so a checkpoint resumes bit for bit)
+  double* rho_out = nullptr;
+  double acc = 0.0;
   __device__ __forceinline__ void begin(double) {}
-  __device__ __forceinline__ void operator()(int q, double v) const {
+  __device__ __forceinline__ void operator()(int q, double v) {
     stcs<T>(LBM_CHECK_ST(base, out + q * nxy, *c), v);
+    if (rho_out) {
+      acc += (double)(T)v;
+      if (q == 26) *rho_out = acc;
+    }
   }
 };
 

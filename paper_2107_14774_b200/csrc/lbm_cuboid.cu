@@ -95,7 +95,9 @@ struct lbm_cuboid {
   bool halo_pending = false;
   bool ghost = false;  // ghost-plane mode (NCCL or fused P2P halo)
   bool paper_rates = false;  // omega_1 = omega_high = 1 -> k_collide_stream_paper
-  bool fd = false;           // FULL_FD: density pass + isotropic gradient
+  bool fd = false;           // FULL_FD / FULL_FD_LAG: density-gradient (lambda, e_rho) terms
+  bool fd_lag = false;       // FULL_FD_LAG: gradient of the stored state's density (d_rho double-buffered,
+                             // written by the collision of the previous step; reading R16b)
   bool fd_fused = true;      // FULL_FD: fused 2.5D kernel (fp64) or density pass + collide (fp32);
                              // env LBM_FD_FUSED=0/1 forces the two-pass / fused path
   bool tma = false;          // TMA-staged collide-stream kernel (cm_tma.cuh); opt-in LBM_TMA=1
@@ -201,7 +203,7 @@ int validate(const lbm_cuboid_params* p) {
   for (int f = 0; f < 6; ++f)
     if (p->bc[f] == LBM_BC_MOVING_WALL && f != 3)
       return fail(LBM_EINVAL, "configuration error: a moving wall is supported on the +y face only (P:L751)");
-  if (p->corrections < 0 || p->corrections > 3) return fail(LBM_EINVAL, "corrections must be an lbm_corr");
+  if (p->corrections < 0 || p->corrections > 4) return fail(LBM_EINVAL, "corrections must be an lbm_corr");
   if (p->precision < 0 || p->precision > 1) return fail(LBM_EINVAL, "precision must be an lbm_prec");
   if (p->halo < 0 || p->halo > 2) return fail(LBM_EINVAL, "halo must be an lbm_halo");
   if (p->graphs < 0 || p->graphs > 3) return fail(LBM_EINVAL, "graphs must be 0, 1, 2 or 3");
@@ -211,8 +213,8 @@ int validate(const lbm_cuboid_params* p) {
   if (p->streaming == LBM_STREAM_AA) {
     if (p->world > 1 || p->halo != LBM_HALO_AUTO)
       return fail(LBM_ENOTSUP, "AA in-place streaming is single-GPU only (no ghost-plane exchange)");
-    if (p->corrections == LBM_CORR_FULL_FD)
-      return fail(LBM_ENOTSUP, "AA in-place streaming does not support FULL_FD");
+    if (p->corrections == LBM_CORR_FULL_FD || p->corrections == LBM_CORR_FULL_FD_LAG)
+      return fail(LBM_ENOTSUP, "AA in-place streaming does not support FULL_FD / FULL_FD_LAG");
   }
   for (int d = 0; d < 3; ++d)
     if (!std::isfinite(p->force[d])) return fail(LBM_EINVAL, "force must be finite");
@@ -266,7 +268,8 @@ void fill_consts(lbm_cuboid* h) {
   c.gx = 3.0 * cs2 - 1.0;
   c.gy = 3.0 * cs2 - c.r2;
   c.gz = 3.0 * cs2 - c.s2;
-  c.galias = (p.corrections == LBM_CORR_FULL_LOCAL || p.corrections == LBM_CORR_FULL_FD) ? 1.0 : 0.0;
+  c.galias = (p.corrections == LBM_CORR_FULL_LOCAL || p.corrections == LBM_CORR_FULL_FD ||
+              p.corrections == LBM_CORR_FULL_FD_LAG) ? 1.0 : 0.0;
   c.corr_on = (p.corrections != LBM_CORR_OFF);
   c.csn = 2.0 * cs2 / p.omega_nu;
   c.csx = 2.0 * cs2 / p.omega_xi;
@@ -343,8 +346,17 @@ lbm::P2PArgs<T> p2p_args(const lbm_cuboid* h, int which, uint32_t epoch) {
   a.flag_up = h->peer_flag_up;
   a.flag_dn = h->peer_flag_dn;
   a.epoch = epoch;
+  // FULL_FD_LAG: the neighbours' density fields of buffer `which` (their ghost planes
+  // receive this slab's boundary-plane densities)
+  const size_t half = size_t(h->nzl + 2) * size_t(h->nxy);
+  a.rho_up = (h->fd_lag && h->peer_rho_up) ? h->peer_rho_up + which * half : nullptr;
+  a.rho_dn = (h->fd_lag && h->peer_rho_dn) ? h->peer_rho_dn + which * half : nullptr;
   return a;
 }
+
+// FULL_FD_LAG: the density field of the state in buf[i] (the lower / upper half
+// of d_rho; population-buffer plane structure with ghost planes)
+double* rho_field(const lbm_cuboid* h, int i) { return h->d_rho + size_t(i) * size_t(h->nzl + 2) * size_t(h->nxy); }
 
 // p2p_which >= 0: fused P2P boundary launch storing into the neighbours' buffer
 // p2p_which and publishing p2p_epoch (LBM_HALO_P2P)
@@ -363,22 +375,29 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
     h->ev_t.push_back({a, b});
     CU(cudaEventRecord(a, s));
   }
+  // FULL_FD_LAG: read the density field of the source state, write the collision's
+  // density into the destination state's field
   const double* rf = h->d_rho;
+  Consts cc = h->c;
+  if (h->fd_lag) {
+    rf = rho_field(h, src == h->buf[0] ? 0 : 1);
+    cc.rf_out = rho_field(h, src == h->buf[0] ? 1 : 0);
+  }
 #define LBM_LAUNCH(KERNEL)                                                                                   \
   do {                                                                                                       \
     if (fp64) {                                                                                              \
       if (h->fd)                                                                                             \
-        lbm::KERNEL<double, true><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, rf, h->c, zbeg, \
+        lbm::KERNEL<double, true><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, rf, cc, zbeg, \
                                                              zstride);                                       \
       else                                                                                                   \
-        lbm::KERNEL<double, false><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, rf, h->c, zbeg, \
+        lbm::KERNEL<double, false><<<g, lbm::kBlock, 0, s>>>((const double*)src, (double*)dst, rf, cc, zbeg, \
                                                               zstride);                                      \
     } else {                                                                                                 \
       if (h->fd)                                                                                             \
-        lbm::KERNEL<float, true><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, rf, h->c, zbeg,    \
+        lbm::KERNEL<float, true><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, rf, cc, zbeg,    \
                                                             zstride);                                        \
       else                                                                                                   \
-        lbm::KERNEL<float, false><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, rf, h->c, zbeg,   \
+        lbm::KERNEL<float, false><<<g, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, rf, cc, zbeg,   \
                                                              zstride);                                       \
     }                                                                                                        \
   } while (0)
@@ -394,13 +413,13 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
   do {                                                                                                       \
     if (h->p.model == LBM_MODEL_RM)                                                                          \
       lbm::k_collide_stream_p2p<T, lbm::CORE_RAW, FD><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, rf,  \
-                                                                                h->c, zbeg, zstride, a);     \
+                                                                                cc, zbeg, zstride, a);     \
     else if (h->paper_rates)                                                                                 \
       lbm::k_collide_stream_p2p<T, lbm::CORE_PAPER, FD><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, rf, \
-                                                                                  h->c, zbeg, zstride, a);   \
+                                                                                  cc, zbeg, zstride, a);   \
     else                                                                                                     \
       lbm::k_collide_stream_p2p<T, lbm::CORE_GENERIC, FD><<<g, lbm::kBlock, 0, s>>>(                         \
-          (const T*)src, (T*)dst, rf, h->c, zbeg, zstride, a);                                               \
+          (const T*)src, (T*)dst, rf, cc, zbeg, zstride, a);                                               \
   } while (0)
   if (p2p_which >= 0) {
     if (fp64)
@@ -417,7 +436,7 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
                   unsigned(nchunks));
     const int kind = (h->p.model == LBM_MODEL_RM) ? lbm::CORE_RAW : (h->paper_rates ? lbm::CORE_PAPER : lbm::CORE_GENERIC);
 #define LBM_FDF(T, K) \
-  lbm::k_collide_stream_fd<T, K><<<gf, lbm::kFdThreads, 0, s>>>((const T*)src, (T*)dst, rf, h->c, zbeg, zst, zlen, zend)
+  lbm::k_collide_stream_fd<T, K><<<gf, lbm::kFdThreads, 0, s>>>((const T*)src, (T*)dst, rf, cc, zbeg, zst, zlen, zend)
     if (fp64) {
       if (kind == lbm::CORE_PAPER) LBM_FDF(double, lbm::CORE_PAPER);
       else if (kind == lbm::CORE_RAW) LBM_FDF(double, lbm::CORE_RAW);
@@ -436,7 +455,7 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
     const int kind = (h->p.model == LBM_MODEL_RM) ? lbm::CORE_RAW : (h->paper_rates ? lbm::CORE_PAPER : lbm::CORE_GENERIC);
 #define LBM_TMAK(T, K)                                                                                          \
   lbm::k_collide_stream_tma<T, K><<<grid, lbm::kTmaThreads, lbm::tma_smem_bytes<T>(), s>>>(maps, (const T*)src, \
-                                                                                          (T*)dst, h->c, tl)
+                                                                                          (T*)dst, cc, tl)
     if (fp64) {
       if (kind == lbm::CORE_PAPER) LBM_TMAK(double, lbm::CORE_PAPER);
       else if (kind == lbm::CORE_RAW) LBM_TMAK(double, lbm::CORE_RAW);
@@ -450,11 +469,11 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
   } else if (h->xpair && !fp64 && !h->fd) {
     const dim3 gp(unsigned((h->nxy / 2 + lbm::kBlock - 1) / lbm::kBlock), unsigned(nplanes), 1);
     if (h->p.model == LBM_MODEL_RM)
-      lbm::k_collide_stream_xpair<lbm::CORE_RAW><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg, zstride);
+      lbm::k_collide_stream_xpair<lbm::CORE_RAW><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, cc, zbeg, zstride);
     else if (h->paper_rates)
-      lbm::k_collide_stream_xpair<lbm::CORE_PAPER><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg, zstride);
+      lbm::k_collide_stream_xpair<lbm::CORE_PAPER><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, cc, zbeg, zstride);
     else
-      lbm::k_collide_stream_xpair<lbm::CORE_GENERIC><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, h->c, zbeg, zstride);
+      lbm::k_collide_stream_xpair<lbm::CORE_GENERIC><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, cc, zbeg, zstride);
   } else if (h->p.model == LBM_MODEL_RM)
     LBM_LAUNCH(k_collide_stream_raw);
   else if (h->paper_rates)
@@ -601,7 +620,7 @@ void drop_graphs(lbm_cuboid* h) {
 }
 
 bool use_persistent(const lbm_cuboid* h) {
-  if (h->ghost || h->aa) return false;
+  if (h->ghost || h->aa || h->fd_lag) return false;
   return h->p.graphs == 3 || (h->p.graphs == 0 && h->nxy * h->nzl <= kPersistMaxNodes);
 }
 
@@ -740,6 +759,16 @@ int exchange(lbm_cuboid* h, int which) {
   if (hp.peer_down >= 0) NC(ncclRecv(b + hp.recv_dn * e, cnt, dt, hp.peer_down, h->comm, h->comm_stream));
   if (hp.peer_down >= 0) NC(ncclSend(b + hp.send_dn * e, cnt, dt, hp.peer_down, h->comm, h->comm_stream));
   if (hp.peer_up >= 0) NC(ncclRecv(b + hp.recv_up * e, cnt, dt, hp.peer_up, h->comm, h->comm_stream));
+  if (h->fd_lag) {
+    // FULL_FD_LAG: the boundary planes of the new state's density field (written by
+    // the boundary launch) into the neighbours' density ghost planes, same order
+    double* r = rho_field(h, which);
+    const size_t n = size_t(h->nxy), nzl = size_t(h->nzl);
+    if (hp.peer_up >= 0) NC(ncclSend(r + nzl * n, n, ncclDouble, hp.peer_up, h->comm, h->comm_stream));
+    if (hp.peer_down >= 0) NC(ncclRecv(r, n, ncclDouble, hp.peer_down, h->comm, h->comm_stream));
+    if (hp.peer_down >= 0) NC(ncclSend(r + n, n, ncclDouble, hp.peer_down, h->comm, h->comm_stream));
+    if (hp.peer_up >= 0) NC(ncclRecv(r + (nzl + 1) * n, n, ncclDouble, hp.peer_up, h->comm, h->comm_stream));
+  }
   NC(ncclGroupEnd());
   CU(cudaEventRecord(h->ev_halo, h->comm_stream));
   h->halo_pending = true;
@@ -844,11 +873,12 @@ int p2p_push(lbm_cuboid* h, int which) {
   int rc;
   if ((rc = p2p_ready(h)) || (rc = p2p_fork(h)) || (rc = p2p_wait(h))) return rc;
   const dim3 g(unsigned((9 * h->nxy + lbm::kBlock - 1) / lbm::kBlock), 2, 1);
+  const double* rsrc = h->fd_lag ? rho_field(h, which) : nullptr;
   if (h->p.precision == LBM_FP64)
-    lbm::k_halo_push<double><<<g, lbm::kBlock, 0, h->comm_stream>>>((const double*)h->buf[which], h->c,
+    lbm::k_halo_push<double><<<g, lbm::kBlock, 0, h->comm_stream>>>((const double*)h->buf[which], rsrc, h->c,
                                                                      p2p_args<double>(h, which, h->epoch + 1));
   else
-    lbm::k_halo_push<float><<<g, lbm::kBlock, 0, h->comm_stream>>>((const float*)h->buf[which], h->c,
+    lbm::k_halo_push<float><<<g, lbm::kBlock, 0, h->comm_stream>>>((const float*)h->buf[which], rsrc, h->c,
                                                                     p2p_args<float>(h, which, h->epoch + 1));
   CU(cudaGetLastError());
   h->launches++;
@@ -876,7 +906,7 @@ int p2p_step(lbm_cuboid* h) {
   }
   if ((rc = p2p_fork(h)) || (rc = p2p_wait(h))) return rc;
   const int nb = (h->nzl > 1) ? 2 : 1;
-  if (h->fd) {
+  if (h->fd && !h->fd_lag) {
     // FULL_FD: publish the same-time density of the boundary planes into the
     // neighbours' density ghost planes first, then wait for theirs
     // planes the boundary-plane collision needs: 0, 1, nz_l - 2, nz_l - 1 (distinct)
@@ -888,7 +918,7 @@ int p2p_step(lbm_cuboid* h) {
       if (!seen) pl.z[np++] = z;
     }
     const dim3 gd = grid_for(h, np);
-    lbm::P2PArgs<double> ra;
+    lbm::P2PArgs<double> ra{};
     ra.up = h->peer_rho_up;
     ra.dn = h->peer_rho_dn;
     ra.counter = h->d_sig + 2;
@@ -956,6 +986,22 @@ int init_kernel(lbm_cuboid* h, const double* rho, const double* u, long long ust
 
 // AA with the moving lid: densities of the lid-row nodes of the stored layout-R
 // state (after init_fields / set_populations) for the first odd step
+// FULL_FD_LAG: density field of the stored state in buf[cur] (after init_fields /
+// set_populations), before its ghost planes are exchanged
+int stored_rho(lbm_cuboid* h) {
+  if (!h->fd_lag) return LBM_OK;
+  const dim3 g = grid_for(h, h->nzl);
+  if (h->p.precision == LBM_FP64)
+    lbm::k_stored_rho<double><<<g, lbm::kBlock, 0, h->stream>>>((const double*)h->buf[h->cur], rho_field(h, h->cur),
+                                                                 h->c, 0);
+  else
+    lbm::k_stored_rho<float><<<g, lbm::kBlock, 0, h->stream>>>((const float*)h->buf[h->cur], rho_field(h, h->cur),
+                                                                h->c, 0);
+  CU(cudaGetLastError());
+  h->launches++;
+  return LBM_OK;
+}
+
 int aa_lid_prep(lbm_cuboid* h) {
   if (!h->d_aa_lid) return LBM_OK;
   const dim3 g(unsigned((h->p.nx + lbm::kBlock - 1) / lbm::kBlock), unsigned(h->nzl), 1);
@@ -994,11 +1040,11 @@ int step_once(lbm_cuboid* h) {
   if (h->p2p) return p2p_step(h);
   NvtxRange nv(h->ghost ? "lbm step (NCCL halo)" : "lbm step");
   if (!h->ghost) {
-    if (h->fd && !h->fd_fused && (rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
+    if (h->fd && !h->fd_lag && !h->fd_fused && (rc = launch_density(h, src, 0, h->nzl, 1, h->stream))) return rc;
     return launch_cs(h, src, dst, 0, h->nzl, 1, h->stream);
   }
   if ((rc = wait_halo(h))) return rc;
-  if (h->fd) {
+  if (h->fd && !h->fd_lag) {
     // same-time density (fused: of the two boundary planes only; the fused
     // kernel forms the rest itself), then the boundary planes to the neighbours
     if (h->fd_fused) {
@@ -1083,7 +1129,8 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->peer_up = hp.peer_up;
   h->peer_down = hp.peer_down;
   h->paper_rates = (p->omega_1 == 1.0 && p->omega_high == 1.0);
-  h->fd = (p->corrections == LBM_CORR_FULL_FD);
+  h->fd = (p->corrections == LBM_CORR_FULL_FD || p->corrections == LBM_CORR_FULL_FD_LAG);
+  h->fd_lag = (p->corrections == LBM_CORR_FULL_FD_LAG);
   // measured at 512^3: fused 9.6 k vs two-pass 9.45 k MLUPS
   // in fp64, but 12.0 k vs 13.9 k with fp32 storage
   h->fd_fused = (p->precision == LBM_FP64);
@@ -1097,6 +1144,7 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   // the P2P step forms only the density planes the boundary collision needs
   // (k_density_p2p); its interior must be the fused kernel, which forms its own
   if (h->p2p && h->fd) h->fd_fused = true;
+  if (h->fd_lag) h->fd_fused = false;  // one collide-stream launch reads the stored density field
   fill_consts(h);
 
   auto bail = [&](int code) {
@@ -1160,7 +1208,7 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
     h->c.aa_lid_rho = h->d_aa_lid;
   }
   if (h->fd) {
-    const size_t rb = size_t(h->nxy) * (h->nzl + 2) * sizeof(double);
+    const size_t rb = size_t(h->nxy) * (h->nzl + 2) * sizeof(double) * (h->fd_lag ? 2 : 1);
     if (cudaMalloc(&h->d_rho, rb) != cudaSuccess || cudaMemsetAsync(h->d_rho, 0, rb, h->stream) != cudaSuccess)
       return bail(fail(LBM_ENOMEM, "cudaMalloc(%zu) for the density field failed", rb));
   }
@@ -1215,7 +1263,7 @@ int lbm_cuboid_init_fields_device(lbm_cuboid_t* h, const double* rho, const doub
   if ((rc = wait_halo(h))) return rc;
   if (h->aa) h->cur = 0;  // AA: the canonical state is written in layout R
   if ((rc = run_init(h, rho, u, (long long)h->nzl * h->nxy, 0, h->nzl))) return rc;
-  if ((rc = aa_lid_prep(h))) return rc;
+  if ((rc = aa_lid_prep(h)) || (rc = stored_rho(h))) return rc;
   return exchange(h, h->cur);
 }
 
@@ -1237,7 +1285,7 @@ int lbm_cuboid_init_fields(lbm_cuboid_t* h, const double* rho, const double* u) 
                          cudaMemcpyHostToDevice, h->stream));
     if ((rc = run_init(h, srho, su, (long long)cnt, z, n))) return rc;
   }
-  if ((rc = aa_lid_prep(h))) return rc;
+  if ((rc = aa_lid_prep(h)) || (rc = stored_rho(h))) return rc;
   CU(cudaStreamSynchronize(h->stream));
   return exchange(h, h->cur);
 }
@@ -1450,7 +1498,7 @@ int lbm_cuboid_set_populations(lbm_cuboid_t* h, const double* f) {
     h->launches++;
     CU(cudaStreamSynchronize(h->stream));
   }
-  if ((rc = aa_lid_prep(h))) return rc;
+  if ((rc = aa_lid_prep(h)) || (rc = stored_rho(h))) return rc;
   return exchange(h, h->cur);
 }
 

@@ -21,7 +21,7 @@ LIB_PATH = os.environ.get("LBM_CUBOID_LIB", os.path.join(_PKG, "liblbm_cuboid.so
 LBM_OK, LBM_EINVAL, LBM_ENOMEM, LBM_ECUDA, LBM_ENCCL, LBM_EUNSTABLE, LBM_ESINGULAR, LBM_ENOTSUP = (
     0, -1, -2, -3, -4, -5, -6, -7)
 BC_PERIODIC, BC_BOUNCE_BACK, BC_MOVING_WALL, BC_FREE_SLIP = 0, 1, 2, 3
-CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF, CORR_FULL_FD = 0, 1, 2, 3
+CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF, CORR_FULL_FD, CORR_FULL_FD_LAG = 0, 1, 2, 3, 4
 FP64, FP32_STORAGE = 0, 1
 HALO_AUTO, HALO_NCCL, HALO_P2P = 0, 1, 2
 P2P_BLOB_BYTES = 512

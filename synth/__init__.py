@@ -21,7 +21,7 @@ import numpy as np
 # boundary types (same integer codes as include/lbm_cuboid.h and the oracle)
 BC_PERIODIC, BC_BOUNCE_BACK, BC_MOVING_WALL, BC_FREE_SLIP = 0, 1, 2, 3
 # correction modes (readings R1)
-CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF, CORR_FULL_FD = 0, 1, 2, 3
+CORR_FULL_LOCAL, CORR_LOW_MACH, CORR_OFF, CORR_FULL_FD, CORR_FULL_FD_LAG = 0, 1, 2, 3, 4
 # storage precision
 PREC_FP64, PREC_FP32 = 0, 1
 # collision model

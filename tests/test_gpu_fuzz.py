@@ -81,7 +81,9 @@ def _draw(rng):
               corrections=int(rng.integers(0, 4)), model=int(rng.integers(0, 2)),
               precision=int(rng.random() < 0.3))
     gpu = dict(graphs=int(rng.integers(0, 4)))
-    fd = kw["corrections"] == synth.CORR_FULL_FD
+    if kw["corrections"] == synth.CORR_FULL_FD and rng.random() < 0.5:
+        kw["corrections"] = synth.CORR_FULL_FD_LAG  # reading R16b (lagged density field)
+    fd = kw["corrections"] in (synth.CORR_FULL_FD, synth.CORR_FULL_FD_LAG)
     roll = rng.random()
     if roll < 0.25 and not fd:
         gpu["streaming"] = 1  # LBM_STREAM_AA: in-place streaming
@@ -140,6 +142,7 @@ def _slab_cases():
         kw, _ = _draw(rng)
         if kw["corrections"] == synth.CORR_FULL_FD:
             continue  # FULL_FD exchanges within a step: slabs on one GPU cannot be stepped one at a time
+            # (FULL_FD_LAG publishes its density with the populations: stepped like the others)
         world = int(rng.choice([2, 3, 4]))
         kw["nz"] = world * int(rng.integers(1, 4))
         out.append((kw, world))

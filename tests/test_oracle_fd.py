@@ -101,3 +101,57 @@ def test_density_gradient_corrections_on_x_axis_of_05_1_lattice():
     """(r,s) = (0.5,1), cs2 = 1/12: the x axis carries 3 cs2 - 1 = -0.75."""
     assert _sound_rate(FD, 0.08, "x", 0.5, 1.0) == pytest.approx(1.0, abs=0.04)
     assert abs(_sound_rate(FULL, 0.08, "x", 0.5, 1.0) - 1.0) > 0.15
+
+
+FD_LAG = 4
+
+
+@pytest.mark.parametrize("model", [0, 1])
+def test_lagged_density_corrections_restore_acoustic_attenuation(model):
+    """Reading R16b (FULL_FD_LAG: the gradient of the stored state's density, one
+    time level behind): the same moving-frame sound attenuation as the same-time
+    density of R16 -- within 1 % of the Navier-Stokes rate along the stretched
+    axis with U_b = 0.1 (FULL_LOCAL: > 8 % off) and at rest."""
+    assert _sound_rate(FD_LAG, 0.1, "z", 1.0, 2.0, model=model) == pytest.approx(1.0, abs=0.01)
+    assert _sound_rate(FD_LAG, 0.0, "z", 1.0, 2.0, model=model) == pytest.approx(1.0, abs=0.01)
+
+
+def test_lagged_density_on_x_axis_of_05_1_lattice():
+    assert _sound_rate(FD_LAG, 0.08, "x", 0.5, 1.0) == pytest.approx(1.0, abs=0.04)
+
+
+def test_lagged_density_is_the_stored_states_density():
+    """The time level of R16b: a stored state whose every node holds density 1
+    (f^eq(1, u) with u varying from node to node: sum_q f^eq = 1 per node) has a
+    zero stored-density gradient, so one FULL_FD_LAG step equals one FULL_LOCAL
+    step (the lambda / e_rho terms vanish with the gradient), while the
+    same-time density of the PULLED populations varies and FULL_FD differs."""
+    r, s = 1.0, 2.0
+    cs2 = synth.auto_cs2(r, s)
+    n = (6, 5, 4)
+    rng = np.random.default_rng(8)
+    u = rng.uniform(-0.05, 0.05, (3, n[2], n[1], n[0]))
+    outs = {}
+    for corr in (FULL, FD, FD_LAG):
+        o = O.Oracle(*n, r, s, cs2, 1.6, omega_xi=1.2, corrections=corr)
+        o.init_fields(np.ones((n[2], n[1], n[0])), u)
+        o.step(1)
+        outs[corr] = o.get_populations()
+    assert np.abs(outs[FD_LAG] - outs[FULL]).max() < 1e-15
+    assert np.abs(outs[FD] - outs[FULL]).max() > 1e-9
+
+
+def test_lagged_density_conserves_mass_and_momentum():
+    """Periodic lattice with a body force: mass constant, momentum + N F per step."""
+    r, s = 0.75, 1.3
+    cs2 = synth.auto_cs2(r, s)
+    F = np.array([2e-5, -1e-5, 3e-5])
+    o = O.Oracle(6, 5, 4, r, s, cs2, 1.5, omega_xi=1.1, force=F, corrections=FD_LAG)
+    rho, u = synth.random_fields(6, 5, 4, 12)
+    o.init_fields(rho, u)
+    e = O.velocities(r, s)
+    f0 = o.get_populations().reshape(27, -1)
+    o.step(5)
+    f1 = o.get_populations().reshape(27, -1)
+    assert abs(f1.sum() - f0.sum()) < 1e-12
+    assert np.allclose(e.T @ f1.sum(axis=1) - e.T @ f0.sum(axis=1), 5 * 120 * F, rtol=0, atol=1e-12)
