@@ -421,7 +421,7 @@ def run_cuda(args):
     if args.streaming == "aa":
         kname = "k_aa (odd/even)"
     if args.corrections == "full_fd":
-        kname = "k_collide_stream_fd" if prec == "fp64" else kname + " + k_density"
+        kname = "k_collide_stream_fd" if os.environ.get("LBM_FD_FUSED") == "1" else kname + " + k_density"
     kfull = f"{kname}<{'double' if prec == 'fp64' else 'float'}>"
     traffic, traffic_src = ncu_traffic(w.name, prec, kfull, nodes_per_launch)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -98,7 +98,7 @@ struct lbm_cuboid {
   bool fd = false;           // FULL_FD / FULL_FD_LAG: density-gradient (lambda, e_rho) terms
   bool fd_lag = false;       // FULL_FD_LAG: gradient of the stored state's density (d_rho double-buffered,
                              // written by the collision of the previous step; reading R16b)
-  bool fd_fused = true;      // FULL_FD: fused 2.5D kernel (fp64) or density pass + collide (fp32);
+  bool fd_fused = true;      // FULL_FD: fused 2.5D kernel or density pass + collide (default since round 2);
                              // env LBM_FD_FUSED=0/1 forces the two-pass / fused path
   bool tma = false;          // TMA-staged collide-stream kernel (cm_tma.cuh); opt-in LBM_TMA=1
   lbm::TmaMaps tmaps[2];     // buf[i] as the 3D tensor (x, y, 27 (nz_l + 2)) for the TMA unit
@@ -1131,9 +1131,10 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->paper_rates = (p->omega_1 == 1.0 && p->omega_high == 1.0);
   h->fd = (p->corrections == LBM_CORR_FULL_FD || p->corrections == LBM_CORR_FULL_FD_LAG);
   h->fd_lag = (p->corrections == LBM_CORR_FULL_FD_LAG);
-  // measured at 512^3: fused 9.6 k vs two-pass 9.45 k MLUPS
-  // in fp64, but 12.0 k vs 13.9 k with fp32 storage
-  h->fd_fused = (p->precision == LBM_FP64);
+  // measured at 512^3: with the FD collide bounded to 80
+  // registers (round 2) the two-pass path is the faster one in both precisions
+  // (fp64 9.9 k vs 9.4 k MLUPS fused; fp32 13.7 k vs 12.0 k)
+  h->fd_fused = false;
   if (const char* e = std::getenv("LBM_FD_FUSED")) h->fd_fused = (std::atoi(e) != 0);
   h->aa = (p->streaming == LBM_STREAM_AA);
   // fp32 storage with an even nx (8-byte aligned node pairs): the x-pair kernel,
