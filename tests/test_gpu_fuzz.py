@@ -11,8 +11,14 @@ cs2 against large c^2, strong non-equilibrium) can make single populations tiny
 or negative; there R12 alone divides the fp32 rounding of the large populations
 (~6e-8 of max|f| per stored value) by a near-zero population, and the floor
 keeps the bar at 1e-7 max|f| (about two fp32 ulps of the largest population).
+Where a draw near the stability limit amplifies fp32 rounding beyond that by
+itself (measured on the oracle: fp64 vs the same oracle rounded to fp32 after
+every step, _fp32_spread), the bar is 4x that intrinsic spread.
 The configurations come from PCG64(2107) so every run checks the same cases
-(LBM_FUZZ_CASES sets how many)."""
+(LBM_FUZZ_CASES sets how many).  A draw whose update is unstable (the oracle's
+state reaches rho <= 0 or |u| > 1, the blow-up criterion of S:L407, or grows
+4x within the 13 steps) is skipped: instability amplifies the two sides'
+rounding differences exponentially."""
 import numpy as np
 import pytest
 
@@ -38,15 +44,48 @@ def P():
     return P
 
 
-def _assert_close(fg, fo, precision, info):
+def _r12(fg, fo):
+    """Reading R12 per population, with a floor at 1e-2 of the largest population."""
+    denom = np.maximum(np.abs(fo), 1e-2 * np.abs(fo).max())
+    return float((np.abs(fg - fo) / denom).max())
+
+
+def _assert_close(fg, fo, precision, info, spread=0.0):
     err = np.abs(fg - fo)
     if precision == 0:
         assert err.max() <= 1e-12, (err.max(), info)
     else:
-        # R12 with a floor at 1e-2 of the largest population
-        denom = np.maximum(np.abs(fo), 1e-2 * np.abs(fo).max())
-        rel = (err / denom).max()
-        assert rel <= 1e-5, (rel, err.max(), info)
+        rel = _r12(fg, fo)
+        assert rel <= max(1e-5, 4.0 * spread), (rel, spread, err.max(), info)
+
+
+def _fp32_spread(kw, f0, steps):
+    """Conditioning of an fp32-storage draw, measured on the oracle alone: the
+    R12 distance between the fp64 oracle and the same oracle whose state is
+    rounded to fp32 after every step (what fp32 storage does).  Near the
+    stability limit a draw can amplify fp32 rounding past R12's 1e-5 by itself
+    (2 of 2,000 draws); there the GPU must stay within 4x of that intrinsic
+    spread instead.  Well-conditioned draws keep the plain 1e-5 bar."""
+    import oracle as O
+
+    a = O.Oracle(**kw)
+    b = O.Oracle(**kw)
+    a.set_populations(f0)
+    b.set_populations(f0.astype(np.float32).astype(np.float64))
+    for _ in range(steps):
+        a.step(1)
+        b.step(1)
+        b.set_populations(b.get_populations().astype(np.float32).astype(np.float64))
+    return _r12(b.get_populations(), a.get_populations())
+
+
+def _stable(o, f0):
+    """The oracle's run stayed bounded: no node with rho <= 0 or |u| > 1 (the
+    blow-up criterion of S:L407) and max|f| grew less than 4x."""
+    rho, u = o.macroscopic()
+    fo = o.get_populations()
+    return bool(np.all(np.isfinite(fo)) and rho.min() > 0 and np.sqrt((u * u).sum(axis=0)).max() <= 1.0 and
+                np.abs(fo).max() < 4 * np.abs(f0).max())
 
 
 def _draw(rng):
@@ -128,8 +167,14 @@ def test_random_problem_matches_oracle(P, i):
     g.sync()  # with the bounds-checked build (LBM_CUBOID_LIB=...lib_debug.so) this reports violations
     fo, fg = o.get_populations(), g.get_populations()
     g.close()
-    assert np.all(np.isfinite(fg))
-    _assert_close(fg, fo, kw["precision"], (kw, gpu))
+    assert np.all(np.isfinite(fg)) or not _stable(o, f0)
+    if not _stable(o, f0):
+        # a draw whose update is unstable (the random rates / cs2 / walls) amplifies
+        # the rounding differences of the two implementations exponentially:
+        # nothing to compare element by element
+        pytest.skip("unstable draw: the oracle's state blows up (S:L407 criterion or 4x growth)")
+    spread = _fp32_spread(kw, f0, steps) if kw["precision"] == 1 else 0.0
+    _assert_close(fg, fo, kw["precision"], (kw, gpu), spread)
 
 
 N_SLAB_CASES = int(os.environ.get("LBM_FUZZ_SLAB_CASES", "40"))
@@ -190,4 +235,7 @@ def test_random_problem_p2p_slabs_match_oracle(P, i):
     for h in hs:
         h.close()
     fo = o.get_populations()
-    _assert_close(fg, fo, kw["precision"], (kw, world))
+    if not _stable(o, f0):
+        pytest.skip("unstable draw: the oracle's state blows up (S:L407 criterion or 4x growth)")
+    spread = _fp32_spread(kw, f0, steps) if kw["precision"] == 1 else 0.0
+    _assert_close(fg, fo, kw["precision"], (kw, world), spread)
