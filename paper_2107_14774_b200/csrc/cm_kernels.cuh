@@ -124,8 +124,8 @@ __device__ __forceinline__ void collide_stream_ab(const T* __restrict__ src, T* 
   double gxr = 0.0, gyr = 0.0, gzr = 0.0;
   if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
   gather<T>(src, c, x, y, z, f);
-  StoreOwn<T> st{dst, dst + (long long)(z + 1) * c.plane + idx, c.nxy, &c,
-                 c.rf_out ? c.rf_out + (long long)(z + 1) * c.nxy + idx : nullptr};
+  StoreOwn<T, FD> st{dst, dst + (long long)(z + 1) * c.plane + idx, c.nxy, &c,
+                     (FD && c.rf_out) ? c.rf_out + (long long)(z + 1) * c.nxy + idx : nullptr};
   run_core<KIND, FD>(c, f, gxr, gyr, gzr, st);
 }
 
@@ -559,9 +559,17 @@ __global__ void LBM_CS_BOUNDS k_aa(T* buf, const __grid_constant__ Consts c, int
     T* p = buf + (long long)(z + 1) * c.plane + idx;
 #pragma unroll
     for (int q = 0; q < 27; ++q) f[q] = ldg(LBM_CHECK_LD(buf, p + q * c.nxy, c));
-    double* lid = (c.aa_lid_rho && y == c.ny - 1) ? c.aa_lid_rho + z * c.nx + x : nullptr;
-    StoreRev<T> st{buf, p, c.nxy, &c, lid, 0.0};
+    StoreRev<T> st{buf, p, c.nxy, &c};
     run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, st);
+    if (c.aa_lid_rho && y == c.ny - 1) {
+      // lid-row node with the moving lid: rho_f = sum of its stored f~ in q order
+      // (the sum the two-buffer gather and k_aa_lid_rho form) for the next odd
+      // step, read back from this thread's own stores (plain, coherent loads)
+      double r0 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 27; ++q) r0 += (double)p[(26 - q) * c.nxy];
+      c.aa_lid_rho[z * c.nx + x] = r0;
+    }
   }
 }
 

@@ -245,23 +245,27 @@ __device__ __forceinline__ void density_gradient(const double* __restrict__ rf, 
 //   StoreRev  (AA even step): own node, slot 26 - q of the same buffer;
 //   StorePush (AA odd step): the slot whose next pull reads it (push with the
 //             wall rules; the exact inverse of gather()).
-template <typename T>
+// RHO (the density-gradient kernels only): also form the node's density for
+// FULL_FD_LAG's next step as the sum of the STORED values in q order (what
+// k_stored_rho forms after a set_populations, so a checkpoint resumes bit for
+// bit); rho_out == nullptr at run time for the same-time FULL_FD.  A
+// compile-time flag, so the plain kernels carry no per-store test.
+template <typename T, bool RHO = false>
 struct StoreOwn {
   T* base;
   T* out;
   int nxy;
   const Consts* c;
-  // FULL_FD_LAG: the node's density for the next step's gradient, formed as the
-  // sum of the STORED values in q order (what k_stored_rho forms after a
-  // set_populations, so a checkpoint resumes bit for bit)
   double* rho_out = nullptr;
   double acc = 0.0;
   __device__ __forceinline__ void begin(double) {}
   __device__ __forceinline__ void operator()(int q, double v) {
     stcs<T>(LBM_CHECK_ST(base, out + q * nxy, *c), v);
-    if (rho_out) {
-      acc += (double)(T)v;
-      if (q == 26) *rho_out = acc;
+    if constexpr (RHO) {
+      if (rho_out) {
+        acc += (double)(T)v;
+        if (q == 26) *rho_out = acc;
+      }
     }
   }
 };
@@ -272,17 +276,9 @@ struct StoreRev {
   T* out;
   int nxy;
   const Consts* c;
-  // lid-row node with the moving lid: rho_f = sum of its stored f~ in q order
-  // (what the two-buffer gather and k_aa_lid_rho sum), for the next odd step
-  double* lid_rho;
-  double acc;
-  __device__ __forceinline__ void begin(double) { acc = 0.0; }
-  __device__ __forceinline__ void operator()(int q, double v) {
+  __device__ __forceinline__ void begin(double) {}
+  __device__ __forceinline__ void operator()(int q, double v) const {
     stcs<T>(LBM_CHECK_ST(base, out + (26 - q) * nxy, *c), v);
-    if (lid_rho) {
-      acc += (double)(T)v;
-      if (q == 26) *lid_rho = acc;
-    }
   }
 };
 
