@@ -3,7 +3,8 @@
 or the -DLBM_DEBUG_BOUNDS build): init (host and device), collide-stream
 (paper-rate, generic, raw; fp64 and fp32), FULL_FD fused and two-pass, all wall
 kinds, ghost-plane NCCL self-exchange, fused P2P halo (self and two in-process
-slabs), graphs, the persistent kernel, AA, macro, pack/unpack, check."""
+slabs), graphs, the persistent kernel, AA, macro, pack/unpack, check; round 2:
+FULL_FD_LAG (all paths), the opt-in TMA and x-pair kernels, the event trace."""
 import os
 import sys
 
@@ -25,7 +26,10 @@ cases = [
     synth.Workload("generic", 9, 7, 5, r=0.75, s=1.3, nu=0.02, omega_1=1.2, omega_high=0.9, init="random"),
     synth.CONFIGS["tgv"].scaled(nx=7, ny=6, nz=5, corrections=synth.CORR_FULL_FD),
     synth.CONFIGS["cavity100"].scaled(nx=6, ny=7, nz=4, corrections=synth.CORR_FULL_FD),
+    synth.CONFIGS["tgv"].scaled(nx=7, ny=6, nz=6, corrections=synth.CORR_FULL_FD_LAG),
+    synth.CONFIGS["cavity100"].scaled(nx=6, ny=7, nz=4, corrections=synth.CORR_FULL_FD_LAG),
 ]
+FD_MODES = (synth.CORR_FULL_FD, synth.CORR_FULL_FD_LAG)
 for w in cases:
     for prec in (0, 1):
         for model in (0, 1):
@@ -34,7 +38,7 @@ for w in cases:
                        {"streaming": 1, "graphs": 2}, {"halo": 2}, {"graphs": 3}, {"fd_two_pass": 1}):
                 if kw.get("halo") and ww.bc[4] != 0:
                     continue
-                if "streaming" in kw and ww.corrections == synth.CORR_FULL_FD:
+                if "streaming" in kw and ww.corrections in FD_MODES:
                     continue
                 if "fd_two_pass" in kw:
                     if ww.corrections != synth.CORR_FULL_FD:
@@ -61,7 +65,7 @@ for w in cases:
                 g.close()
                 os.environ.pop("LBM_FD_FUSED", None)
             # two P2P slabs in this process, stepped one at a time (remote ghost stores)
-            if ww.nz % 2 == 0 and ww.corrections != synth.CORR_FULL_FD:
+            if ww.nz % 2 == 0 and ww.corrections != synth.CORR_FULL_FD:  # FULL_FD_LAG included
                 hs = [P.Lattice(**ww.params(), rank=r, world=2, halo=2) for r in range(2)]
                 blobs = [h.p2p_export() for h in hs]
                 for h in hs:
@@ -78,5 +82,24 @@ for w in cases:
                         h.sync()
                 for h in hs:
                     h.close()
+# opt-in kernels: TMA-staged (rows of >= 128 nodes) and x-pair (fp32, nx even), with walls
+# and periodic faces, plus the event trace
+for env, ws in (("LBM_TMA", [synth.CONFIGS["tgv"].scaled(nx=136, ny=5, nz=4),
+                             synth.CONFIGS["cavity100"].scaled(nx=128, ny=5, nz=4)]),
+                ("LBM_XPAIR", [synth.CONFIGS["tgv"].scaled(nx=70, ny=5, nz=4, precision=1),
+                               synth.CONFIGS["cavity100"].scaled(nx=66, ny=5, nz=4, precision=1)])):
+    os.environ[env] = "1"
+    for w in ws:
+        for prec in ((0, 1) if env == "LBM_TMA" else (1,)):
+            g = P.Lattice(**w.scaled(precision=prec).params())
+            rho, u = synth.random_fields(w.nx, w.ny, w.nz, 7)
+            g.init_fields(rho, u)
+            g.trace(True)
+            g.step(6)
+            g.trace_read()
+            g.trace(False)
+            g.sync()
+            g.close()
+    os.environ.pop(env)
 torch.cuda.synchronize()
 print("sanitize_run: all kernels exercised")
