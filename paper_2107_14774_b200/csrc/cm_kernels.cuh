@@ -110,13 +110,14 @@ __device__ __forceinline__ double ring_rho(const T* src, const double* rf, const
 // ------------------------------------------------ the fused kernels (two buffers)
 // One thread per node of planes zbeg + i*zstride, i < gridDim.y, of the local
 // slab: pull (gather) from src, collide, store at the own node of dst.
-template <typename T, int KIND, bool FD>
+// SNX > 0: the plane width is the compile-time SNX (k_collide_stream_paper_shape)
+template <typename T, int KIND, bool FD, int SNX = 0>
 __device__ __forceinline__ void collide_stream_ab(const T* __restrict__ src, T* __restrict__ dst,
                                                   const double* __restrict__ rf, const Consts& c, int zbeg,
                                                   int zstride) {
   const int idx = blockIdx.x * kBlock + threadIdx.x;
   if (idx >= c.nxy) return;
-  const int y = row_of(c, idx);
+  const int y = SNX ? idx / SNX : row_of(c, idx);
   const int x = idx - y * c.nx;
   const int z = zbeg + blockIdx.y * zstride;  // zstride > 1: the two boundary planes in one launch
   double f[27];
@@ -141,6 +142,29 @@ __global__ void LBM_CS_BOUNDS_FD(FD) k_collide_stream_paper(const T* __restrict_
                                                      const double* __restrict__ rf, const __grid_constant__ Consts c,
                                                      int zbeg, int zstride) {
   collide_stream_ab<T, CORE_PAPER, FD>(src, dst, rf, c, zbeg, zstride);
+}
+
+// Plane-shape specialisation of the paper-rate kernel (the default collision of
+// every BASELINE configuration): with nx and ny compile-time constants every
+// pull-source and store offset of the warp-uniform interior path is a constant,
+// which the loads and stores carry as immediates (27 LDG + 8 integer
+// instructions per node instead of 27 LDG + ~160; cuobjdump), the rest of the
+// code is the same inlined collide_stream_ab, so results are bitwise those of
+// k_collide_stream_paper (also with the density-gradient terms: FD, whose
+// 26-neighbour density stencil gets immediate offsets too).  Instantiated for the
+// plane shapes of the BASELINE configs 3-5 (lbm_cuboid.cu, launch_cs); other
+// shapes use the general kernel.
+template <typename T, int SNX, int SNY, bool FD>
+__global__ void LBM_CS_BOUNDS_FD(FD) k_collide_stream_paper_shape(const T* __restrict__ src, T* __restrict__ dst,
+                                                                  const double* __restrict__ rf,
+                                                                  const __grid_constant__ Consts c0, int zbeg,
+                                                                  int zstride) {
+  Consts c = c0;
+  c.nx = SNX;
+  c.ny = SNY;
+  c.nxy = SNX * SNY;
+  c.plane = 27LL * SNX * SNY;
+  collide_stream_ab<T, CORE_PAPER, FD, SNX>(src, dst, rf, c, zbeg, zstride);
 }
 
 template <typename T, bool FD>

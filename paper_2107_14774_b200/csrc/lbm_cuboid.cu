@@ -100,6 +100,7 @@ struct lbm_cuboid {
                              // written by the collision of the previous step; reading R16b)
   bool fd_fused = true;      // FULL_FD: fused 2.5D kernel or density pass + collide (default since round 2);
                              // env LBM_FD_FUSED=0/1 forces the two-pass / fused path
+  bool shape_spec = false;   // plane shape compiled in (k_collide_stream_paper_shape); env LBM_SHAPE_SPEC=0 disables
   bool tma = false;          // TMA-staged collide-stream kernel (cm_tma.cuh); opt-in LBM_TMA=1
   lbm::TmaMaps tmaps[2];     // buf[i] as the 3D tensor (x, y, 27 (nz_l + 2)) for the TMA unit
   int tma_grid = 0;          // persistent grid size of the TMA kernel (resident CTAs)
@@ -474,6 +475,31 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
       lbm::k_collide_stream_xpair<lbm::CORE_PAPER><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, cc, zbeg, zstride);
     else
       lbm::k_collide_stream_xpair<lbm::CORE_GENERIC><<<gp, lbm::kBlock, 0, s>>>((const float*)src, (float*)dst, cc, zbeg, zstride);
+  } else if (h->shape_spec && (!h->fd || !h->fd_fused) && h->paper_rates && h->p.model == LBM_MODEL_CM) {
+    // compile-time plane shape (k_collide_stream_paper_shape); FULL_FD two-pass and FULL_FD_LAG too
+#define LBM_SHAPE(T, NX, NY)                                                                                     \
+  do {                                                                                                           \
+    if (h->fd)                                                                                                   \
+      lbm::k_collide_stream_paper_shape<T, NX, NY, true><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, rf,  \
+                                                                                  cc, zbeg, zstride);          \
+    else                                                                                                         \
+      lbm::k_collide_stream_paper_shape<T, NX, NY, false><<<g, lbm::kBlock, 0, s>>>((const T*)src, (T*)dst, rf, \
+                                                                                   cc, zbeg, zstride);         \
+  } while (0)
+#define LBM_SHAPES(T)                                                              \
+  do {                                                                             \
+    const int nx_ = h->p.nx, ny_ = h->p.ny;                                        \
+    if (nx_ == 512 && ny_ == 512) LBM_SHAPE(T, 512, 512);                          \
+    else if (nx_ == 256 && ny_ == 256) LBM_SHAPE(T, 256, 256);                     \
+    else if (nx_ == 512 && ny_ == 256) LBM_SHAPE(T, 512, 256);                     \
+    else LBM_SHAPE(T, 1024, 1024);                                                 \
+  } while (0)
+    if (fp64)
+      LBM_SHAPES(double);
+    else
+      LBM_SHAPES(float);
+#undef LBM_SHAPES
+#undef LBM_SHAPE
   } else if (h->p.model == LBM_MODEL_RM)
     LBM_LAUNCH(k_collide_stream_raw);
   else if (h->paper_rates)
@@ -1137,6 +1163,10 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
   h->fd_fused = false;
   if (const char* e = std::getenv("LBM_FD_FUSED")) h->fd_fused = (std::atoi(e) != 0);
   h->aa = (p->streaming == LBM_STREAM_AA);
+  // plane shapes of the BASELINE configs 3-5 with a compiled-in specialisation
+  h->shape_spec = (p->nx == 512 && p->ny == 512) || (p->nx == 256 && p->ny == 256) ||
+                  (p->nx == 512 && p->ny == 256) || (p->nx == 1024 && p->ny == 1024);
+  if (const char* e = std::getenv("LBM_SHAPE_SPEC")) h->shape_spec = h->shape_spec && (std::atoi(e) != 0);
   // fp32 storage with an even nx (8-byte aligned node pairs): the x-pair kernel,
   // opt-in (LBM_XPAIR=1): measured no faster than one node per thread
   const char* xp = std::getenv("LBM_XPAIR");
