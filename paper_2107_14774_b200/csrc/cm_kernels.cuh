@@ -124,7 +124,31 @@ __device__ __forceinline__ void collide_stream_ab(const T* __restrict__ src, T* 
   // FULL_FD: gradient first, so its L2-resident loads overlap the population loads
   double gxr = 0.0, gyr = 0.0, gzr = 0.0;
   if (FD) density_gradient(rf, c, x, y, z, gxr, gyr, gzr);
-  gather<T>(src, c, x, y, z, f);
+  bool interior = false;
+  if (SNX > 0 && SNX % 32 == 0) {
+    // compile-time plane width, a multiple of the warp: a warp is 32 nodes of one
+    // row, so the warp-uniform interior test of gather() reduces to the warp's
+    // first x, its row and its plane -- decided before any per-lane source index
+    // is formed (the general prologue costs ~100 instructions per node)
+    const int x0 = x & ~31;
+    interior = x0 > 0 && x0 + 32 < SNX && y > 0 && y < c.ny - 1 &&
+               !(z == 0 && (c.face[4] == FK_WRAP || (c.face[4] >= FK_BOUNCE && c.face[4] <= FK_SLIP))) &&
+               !(z == c.nzl - 1 && (c.face[5] == FK_WRAP || (c.face[5] >= FK_BOUNCE && c.face[5] <= FK_SLIP)));
+  }
+  if (interior) {
+    const T* b = src + (long long)(z + 1) * c.plane + idx;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int q = LBM_Q(i, j, k);
+          f[q] = ldg(LBM_CHECK_LD(src, b + ((long long)(1 - k) * c.plane + (q * c.nxy + (1 - j) * c.nx + (1 - i))), c));
+        }
+  } else {
+    gather<T>(src, c, x, y, z, f);
+  }
   StoreOwn<T, FD> st{dst, dst + (long long)(z + 1) * c.plane + idx, c.nxy, &c,
                      (FD && c.rf_out) ? c.rf_out + (long long)(z + 1) * c.nxy + idx : nullptr};
   run_core<KIND, FD>(c, f, gxr, gyr, gzr, st);
