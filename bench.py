@@ -416,13 +416,7 @@ def run_cuda(args):
     peak, peak_src = measured_peaks()
     achieved = bpn * nodes_per_launch / (kernel_ms * 1e-3) / 1e9
     prec = "fp64" if w.precision == 0 else "fp32"
-    kname = ("k_collide_stream_raw" if w.model == synth.MODEL_RM else
-             "k_collide_stream_paper" if lat.info()["paper_rate_kernel"] else "k_collide_stream")
-    if args.streaming == "aa":
-        kname = "k_aa (odd/even)"
-    if args.corrections == "full_fd":
-        kname = "k_collide_stream_fd" if os.environ.get("LBM_FD_FUSED") == "1" else kname + " + k_density"
-    kfull = f"{kname}<{'double' if prec == 'fp64' else 'float'}>"
+    kfull = lat.kernel_name()
     traffic, traffic_src = ncu_traffic(w.name, prec, kfull, nodes_per_launch)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "traffic_source": traffic_src, "source_hash": kernel_source_hash(),

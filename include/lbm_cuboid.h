@@ -268,6 +268,12 @@ int lbm_cuboid_info(const lbm_cuboid_t *h, int64_t out[8]);
 /* cudaStream_t of the compute stream (for event timing by the caller). */
 void *lbm_cuboid_stream(const lbm_cuboid_t *h);
 
+/* Name of the collide-stream kernel this handle's steps launch (e.g.
+ * "k_collide_stream_paper_shape<double,512,512>"; "+ k_density" for the
+ * two-pass FULL_FD), for profiles and the bench's roofline record.  Valid until
+ * the next call on the handle; "" for NULL. */
+const char *lbm_cuboid_kernel_name(const lbm_cuboid_t *h);
+
 /* The handle's NCCL communicator (ghost-plane exchange with LBM_HALO_AUTO at
  * world > 1, or LBM_HALO_NCCL): out[0] = ncclCommCount, out[1] = this rank in
  * it (ncclCommUserRank); both -1 when the handle has no communicator (single

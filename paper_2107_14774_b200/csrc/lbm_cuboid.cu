@@ -100,6 +100,7 @@ struct lbm_cuboid {
                              // written by the collision of the previous step; reading R16b)
   bool fd_fused = true;      // FULL_FD: fused 2.5D kernel or density pass + collide (default since round 2);
                              // env LBM_FD_FUSED=0/1 forces the two-pass / fused path
+  std::string kname;         // lbm_cuboid_kernel_name
   bool shape_spec = false;   // plane shape compiled in (k_collide_stream_paper_shape); env LBM_SHAPE_SPEC=0 disables
   bool tma = false;          // TMA-staged collide-stream kernel (cm_tma.cuh); opt-in LBM_TMA=1
   lbm::TmaMaps tmaps[2];     // buf[i] as the 3D tensor (x, y, 27 (nz_l + 2)) for the TMA unit
@@ -1570,6 +1571,31 @@ int lbm_cuboid_info(const lbm_cuboid_t* h, int64_t out[8]) {
 }
 
 void* lbm_cuboid_stream(const lbm_cuboid_t* h) { return h ? (void*)h->stream : nullptr; }
+
+const char* lbm_cuboid_kernel_name(const lbm_cuboid_t* h) {
+  if (!h) return "";
+  const char* t = (h->p.precision == LBM_FP64) ? "double" : "float";
+  std::string k;
+  if (h->aa) {
+    k = std::string("k_aa<") + t + ">";
+  } else if (h->fd && h->fd_fused && !h->p2p) {
+    k = std::string("k_collide_stream_fd<") + t + ">";
+  } else if (h->tma && !h->fd) {
+    k = std::string("k_collide_stream_tma<") + t + ">";
+  } else if (h->xpair && h->p.precision != LBM_FP64 && !h->fd) {
+    k = "k_collide_stream_xpair<float>";
+  } else if (h->shape_spec && h->paper_rates && h->p.model == LBM_MODEL_CM) {
+    k = std::string("k_collide_stream_paper_shape<") + t + "," + std::to_string(h->p.nx) + "," +
+        std::to_string(h->p.ny) + ">";
+  } else {
+    k = (h->p.model == LBM_MODEL_RM) ? "k_collide_stream_raw<" : (h->paper_rates ? "k_collide_stream_paper<"
+                                                                                   : "k_collide_stream<");
+    k = k + t + ">";
+  }
+  if (h->fd && !h->fd_lag && !h->fd_fused) k += " + k_density";
+  const_cast<lbm_cuboid_t*>(h)->kname = k;
+  return h->kname.c_str();
+}
 
 int lbm_cuboid_comm_ranks(const lbm_cuboid_t* h, int32_t out[2]) {
   if (!h || !out) return fail(LBM_EINVAL, "NULL argument");

@@ -35,7 +35,7 @@ EXPORTS = ["lbm_cuboid_default_params", "lbm_cuboid_buffer_bytes", "lbm_cuboid_h
            "lbm_cuboid_step", "lbm_cuboid_sync", "lbm_cuboid_get_macroscopic",
            "lbm_cuboid_get_macroscopic_device", "lbm_cuboid_get_populations",
            "lbm_cuboid_get_populations_planes", "lbm_cuboid_set_populations", "lbm_cuboid_check", "lbm_cuboid_set_force",
-           "lbm_cuboid_info", "lbm_cuboid_stream", "lbm_cuboid_comm_ranks", "lbm_cuboid_timing", "lbm_cuboid_timing_read",
+           "lbm_cuboid_info", "lbm_cuboid_stream", "lbm_cuboid_comm_ranks", "lbm_cuboid_kernel_name", "lbm_cuboid_timing", "lbm_cuboid_timing_read",
            "lbm_cuboid_trace", "lbm_cuboid_trace_read",
            "lbm_cuboid_destroy", "lbm_cuboid_last_error"]
 
@@ -97,6 +97,8 @@ def load():
     L.lbm_cuboid_stream.restype = _VP
     L.lbm_cuboid_comm_ranks.argtypes = [_VP, ctypes.POINTER(ctypes.c_int32)]
     L.lbm_cuboid_comm_ranks.restype = ctypes.c_int
+    L.lbm_cuboid_kernel_name.argtypes = [_VP]
+    L.lbm_cuboid_kernel_name.restype = ctypes.c_char_p
     L.lbm_cuboid_trace.argtypes = [_VP, ctypes.c_int]
     L.lbm_cuboid_trace.restype = ctypes.c_int
     L.lbm_cuboid_trace_read.argtypes = [_VP, _D, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)]
@@ -321,6 +323,10 @@ class Lattice:
         kinds = {0: "collide", 1: "boundary", 2: "nccl_halo", 3: "density"}
         return [{"kind": kinds[int(r[0])], "stream": "compute" if r[1] == 0 else "halo", "zbeg": int(r[2]),
                  "nplanes": int(r[3]), "t0_ms": float(r[4]), "t1_ms": float(r[5])} for r in a[:n.value]]
+
+    def kernel_name(self) -> str:
+        """The collide-stream kernel this lattice's steps launch."""
+        return load().lbm_cuboid_kernel_name(self._h).decode()
 
     def comm_ranks(self):
         """(nranks, rank) of the library's NCCL communicator, (-1, -1) without one."""

@@ -71,3 +71,20 @@ def test_shape_kernel_with_density_gradient_terms(P, case, corr, monkeypatch):
     assert np.array_equal(a.get_populations(), b.get_populations())
     a.close()
     b.close()
+
+
+def test_kernel_name_reports_the_launched_variant(P, monkeypatch):
+    w = CASES["tgv_512x512"]
+    g = P.Lattice(**w.params())
+    assert g.kernel_name() == "k_collide_stream_paper_shape<double,512,512>"
+    g.close()
+    g = P.Lattice(**w.scaled(nx=96, ny=40, precision=1).params())
+    assert g.kernel_name() == "k_collide_stream_paper<float>"
+    g.close()
+    g = P.Lattice(**w.scaled(nx=96, ny=40, corrections=synth.CORR_FULL_FD).params())
+    assert g.kernel_name() == "k_collide_stream_paper<double> + k_density"
+    g.close()
+    monkeypatch.setenv("LBM_SHAPE_SPEC", "0")
+    g = P.Lattice(**w.params(), model=1)
+    assert g.kernel_name() == "k_collide_stream_raw<double>"
+    g.close()
