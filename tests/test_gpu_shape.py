@@ -85,6 +85,6 @@ def test_kernel_name_reports_the_launched_variant(P, monkeypatch):
     assert g.kernel_name() == "k_collide_stream_paper<double> + k_density"
     g.close()
     monkeypatch.setenv("LBM_SHAPE_SPEC", "0")
-    g = P.Lattice(**w.params(), model=1)
+    g = P.Lattice(**w.scaled(model=1).params())
     assert g.kernel_name() == "k_collide_stream_raw<double>"
     g.close()
