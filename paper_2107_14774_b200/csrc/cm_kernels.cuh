@@ -621,6 +621,74 @@ __global__ void LBM_CS_BOUNDS k_aa(T* buf, const __grid_constant__ Consts c, int
   }
 }
 
+// Plane-shape specialisation of the AA kernels (paper rates; see
+// k_collide_stream_paper_shape): with nx, ny compile-time, a warp of 32 nodes in
+// the interior of its row and plane pulls from reversed slots and pushes to
+// x + e_q at constant offsets (immediates); other warps take the general code.
+template <typename T>
+struct StorePushInterior {  // AA odd step, interior node: f~_q(x) -> slot q of node x + e_q
+  T* own;                   // slot 0 of the node itself (plane z)
+  const Consts* c;
+  T* base;
+  __device__ __forceinline__ void begin(double) {}
+  __device__ __forceinline__ void operator()(int q, double v) const {
+    const int i = q % 3, j = (q / 3) % 3, k = q / 9;
+    stcs<T>(LBM_CHECK_ST(base, own + ((long long)(k - 1) * c->plane + (q * c->nxy + (j - 1) * c->nx + (i - 1))), *c),
+            v);
+  }
+};
+
+template <typename T, bool ODD, int SNX, int SNY>
+__global__ void LBM_CS_BOUNDS k_aa_shape(T* buf, const __grid_constant__ Consts c0, int zbeg, int zstride) {
+  Consts c = c0;
+  c.nx = SNX;
+  c.ny = SNY;
+  c.nxy = SNX * SNY;
+  c.plane = 27LL * SNX * SNY;
+  const int idx = blockIdx.x * kBlock + threadIdx.x;
+  if (idx >= c.nxy) return;
+  const int y = idx / SNX;
+  const int x = idx - y * SNX;
+  const int z = zbeg + blockIdx.y * zstride;
+  if (!ODD) {  // the even step has no neighbour addressing: the general code is already constant-offset
+    T* p = buf + (long long)(z + 1) * c.plane + idx;
+    double f[27];
+#pragma unroll
+    for (int q = 0; q < 27; ++q) f[q] = ldg(LBM_CHECK_LD(buf, p + q * c.nxy, c));
+    StoreRev<T> st{buf, p, c.nxy, &c};
+    run_core<CORE_PAPER, false>(c, f, 0.0, 0.0, 0.0, st);
+    if (c.aa_lid_rho && y == c.ny - 1) {
+      double r0 = 0.0;
+#pragma unroll
+      for (int q = 0; q < 27; ++q) r0 += (double)p[(26 - q) * c.nxy];
+      c.aa_lid_rho[z * c.nx + x] = r0;
+    }
+    return;
+  }
+  const int x0 = x & ~31;
+  const bool interior = (SNX % 32 == 0) && x0 > 0 && x0 + 32 < SNX && y > 0 && y < SNY - 1 && z > 0 &&
+                        z < c.nzl - 1;
+  double f[27];
+  if (interior) {
+    T* b = buf + (long long)(z + 1) * c.plane + idx;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int q = LBM_Q(i, j, k);
+          f[q] = ldg(LBM_CHECK_LD(buf, b + ((long long)(1 - k) * c.plane + ((26 - q) * c.nxy + (1 - j) * SNX + (1 - i))), c));
+        }
+    StorePushInterior<T> st{b, &c, buf};
+    run_core<CORE_PAPER, false>(c, f, 0.0, 0.0, 0.0, st);
+  } else {
+    gather<T, true>(buf, c, x, y, z, f);
+    StorePush<T> st(buf, c, x, y, z);
+    run_core<CORE_PAPER, false>(c, f, 0.0, 0.0, 0.0, st);
+  }
+}
+
 // AA with the moving lid, after init_fields / set_populations (layout R): the
 // density sum f~ of every lid-row node for the first odd step (see gather<REV>).
 template <typename T>

@@ -543,7 +543,26 @@ int launch_aa(lbm_cuboid* h, cudaStream_t s) {
     else                                                                                               \
       lbm::k_aa<T, K, false><<<g, lbm::kBlock, 0, s>>>((T*)h->buf[0], h->c, 0, 1);                   \
   } while (0)
-  if (fp64) {
+#define LBM_AAS(T, NX, NY)                                                                              \
+  do {                                                                                                  \
+    if (odd)                                                                                            \
+      lbm::k_aa_shape<T, true, NX, NY><<<g, lbm::kBlock, 0, s>>>((T*)h->buf[0], h->c, 0, 1);          \
+    else                                                                                                \
+      lbm::k_aa_shape<T, false, NX, NY><<<g, lbm::kBlock, 0, s>>>((T*)h->buf[0], h->c, 0, 1);         \
+  } while (0)
+#define LBM_AASHAPES(T)                                                                                 \
+  do {                                                                                                  \
+    if (h->p.nx == 512 && h->p.ny == 512) LBM_AAS(T, 512, 512);                                         \
+    else if (h->p.nx == 256 && h->p.ny == 256) LBM_AAS(T, 256, 256);                                    \
+    else if (h->p.nx == 512 && h->p.ny == 256) LBM_AAS(T, 512, 256);                                    \
+    else LBM_AAS(T, 1024, 1024);                                                                        \
+  } while (0)
+  if (h->shape_spec && kind == lbm::CORE_PAPER && h->p.model == LBM_MODEL_CM) {
+    if (fp64)
+      LBM_AASHAPES(double);
+    else
+      LBM_AASHAPES(float);
+  } else if (fp64) {
     if (kind == lbm::CORE_PAPER) LBM_AA(double, lbm::CORE_PAPER);
     else if (kind == lbm::CORE_RAW) LBM_AA(double, lbm::CORE_RAW);
     else LBM_AA(double, lbm::CORE_GENERIC);
@@ -552,6 +571,8 @@ int launch_aa(lbm_cuboid* h, cudaStream_t s) {
     else if (kind == lbm::CORE_RAW) LBM_AA(float, lbm::CORE_RAW);
     else LBM_AA(float, lbm::CORE_GENERIC);
   }
+#undef LBM_AASHAPES
+#undef LBM_AAS
 #undef LBM_AA
   CU(cudaGetLastError());
   if (timed) {
@@ -1577,7 +1598,9 @@ const char* lbm_cuboid_kernel_name(const lbm_cuboid_t* h) {
   const char* t = (h->p.precision == LBM_FP64) ? "double" : "float";
   std::string k;
   if (h->aa) {
-    k = std::string("k_aa<") + t + ">";
+    k = (h->shape_spec && h->paper_rates && h->p.model == LBM_MODEL_CM)
+            ? std::string("k_aa_shape<") + t + "," + std::to_string(h->p.nx) + "," + std::to_string(h->p.ny) + ">"
+            : std::string("k_aa<") + t + ">";
   } else if (h->fd && h->fd_fused && !h->p2p) {
     k = std::string("k_collide_stream_fd<") + t + ">";
   } else if (h->tma && !h->fd) {

@@ -88,3 +88,26 @@ def test_kernel_name_reports_the_launched_variant(P, monkeypatch):
     g = P.Lattice(**w.scaled(model=1).params())
     assert g.kernel_name() == "k_collide_stream_raw<double>"
     g.close()
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("case", ["cavity_256x256", "shear_512x256", "tgv_512x512"])
+def test_shape_aa_kernels_bitwise_equal_general(P, case, prec, monkeypatch):
+    """AA in-place streaming through k_aa_shape (interior warps pull reversed
+    slots and push at constant offsets) against the general AA kernels, after
+    an odd and an even number of steps (both layouts), lid included."""
+    w = CASES[case].scaled(precision=prec)
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 90)
+    monkeypatch.setenv("LBM_SHAPE_SPEC", "0")
+    a = P.Lattice(**w.params(), streaming=1, graphs=1)
+    monkeypatch.delenv("LBM_SHAPE_SPEC")
+    b = P.Lattice(**w.params(), streaming=1, graphs=1)
+    assert b.kernel_name().startswith("k_aa_shape<")
+    for g in (a, b):
+        g.init_fields(rho, u)
+    for n in (5, 6):
+        a.step(n)
+        b.step(n)
+        assert np.array_equal(a.get_populations(), b.get_populations()), n
+    a.close()
+    b.close()
