@@ -323,12 +323,15 @@ __global__ void __launch_bounds__(kBlock, KIND == CORE_PAPER ? LBM_XP_MINB : 3) 
 // chunk blockIdx.z covers planes [z0, z1), z0 = zbeg + blockIdx.z * zstride,
 // z1 = min(z0 + zlen, zend).  Iteration p forms rho(p) on the tile and its ring,
 // then collides plane p - 1.
-template <typename T, int KIND>
+// srho: the CTA's four-plane density ring; sync: the barrier of the kFdThreads
+// threads that run this (the whole CTA, or the consumer warps of the TMA kernel)
+typedef double FdRho[kFdTy + 2][kFdRw];
+template <typename T, int KIND, class Sync>
 __device__ __forceinline__ void collide_stream_fd_fused(const T* __restrict__ src, T* __restrict__ dst,
                                                         const double* __restrict__ rf, const Consts& c, int zbeg,
-                                                        int zstride, int zlen, int zend) {
-  __shared__ double srho[4][kFdTy + 2][kFdRw];
-  const int tx = threadIdx.x % kFdTx, ty = threadIdx.x / kFdTx;
+                                                        int zstride, int zlen, int zend, FdRho* srho, Sync sync,
+                                                        int tid) {
+  const int tx = tid % kFdTx, ty = tid / kFdTx;
   const int x0 = blockIdx.x * kFdTx, y0 = blockIdx.y * kFdTy;
   const int z0 = zbeg + blockIdx.z * zstride;
   const int z1 = min(z0 + zlen, zend);
@@ -337,11 +340,11 @@ __device__ __forceinline__ void collide_stream_fd_fused(const T* __restrict__ sr
   for (int p = z0 - 1; p <= z1; ++p) {
     // four slots: the slot written here was last read two planes ago, and this
     // iteration's barrier separates the two (one barrier per plane)
-    for (int pos = threadIdx.x; pos < kFdRing; pos += kFdThreads) {
+    for (int pos = tid; pos < kFdRing; pos += kFdThreads) {
       const int ly = pos / kFdRw, lx = pos - ly * kFdRw;
       srho[p & 3][ly][lx] = ring_rho<T>(src, rf, c, x0 + lx - 1, y0 + ly - 1, p);
     }
-    __syncthreads();
+    sync();
     if (p > z0 && active) {
       const int z = p - 1;
       double gxr, gyr, gzr;
@@ -360,7 +363,9 @@ template <typename T, int KIND>
 __global__ void __launch_bounds__(kFdThreads, LBM_FD_MINB)
     k_collide_stream_fd(const T* __restrict__ src, T* __restrict__ dst, const double* __restrict__ rf,
                         const __grid_constant__ Consts c, int zbeg, int zstride, int zlen, int zend) {
-  collide_stream_fd_fused<T, KIND>(src, dst, rf, c, zbeg, zstride, zlen, zend);
+  __shared__ double srho[4][kFdTy + 2][kFdRw];
+  collide_stream_fd_fused<T, KIND>(src, dst, rf, c, zbeg, zstride, zlen, zend, srho, [] { __syncthreads(); },
+                                   int(threadIdx.x));
 }
 
 // ------------------------------------ fused collide-stream + peer-memory halo (P2P)

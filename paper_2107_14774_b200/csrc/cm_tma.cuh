@@ -37,6 +37,7 @@
 #include <cuda.h>
 
 #include "cm_common.cuh"
+#include "cm_kernels.cuh"
 #include "cm_moments.cuh"
 #include "cm_stream.cuh"
 
@@ -53,6 +54,15 @@ namespace lbm {
 #endif
 #ifndef LBM_TMA_MINB
 #define LBM_TMA_MINB 3  // 3 x 160 threads: 136 registers (4: 96 with spills, measured slower)
+#endif
+#ifndef LBM_FD_TMA_STAGES
+#define LBM_FD_TMA_STAGES 2  // FULL_FD TMA kernel: stages of the ring (one read, one in flight)
+#endif
+#ifndef LBM_FD_TMA_MINB64
+#define LBM_FD_TMA_MINB64 2  // resident CTAs per SM (fp64: 2 x 103 KB of shared memory)
+#endif
+#ifndef LBM_FD_TMA_MINB32
+#define LBM_FD_TMA_MINB32 2
 #endif
 #ifndef LBM_TMA_WRAPBOX32
 #define LBM_TMA_WRAPBOX32 1  // fp32: stage the x-wrap column with wrap boxes
@@ -272,6 +282,203 @@ __global__ void __launch_bounds__(kTmaThreads, LBM_TMA_MINB)
     }
     StoreOwn<T> st{dst, dst + (long long)(z + 1) * c.plane + (y * c.nx + x), c.nxy, &c};
     run_core<KIND, false>(c, f, 0.0, 0.0, 0.0, st);
+  }
+}
+
+// ------------------------------------------------ TMA-staged fused FULL_FD kernel
+// The 2.5D march of collide_stream_fd_fused (cm_kernels.cuh; FULL_FD's
+// same-time density) with the pulled populations of each
+// plane staged by the TMA unit instead of gathered per thread from L2.
+//
+// A CTA owns the kFdTx x kFdTy tile (x0, y0) of one z-chunk; iteration p of the
+// march needs the pulled populations of plane p on the tile and its one-node
+// ring, X in [x0 - 1, x0 + kFdTx], Y in [y0 - 1, y0 + kFdTy].  For direction
+// q = (e_x, e_y, e_z) they are the elements (X - e_x, Y - e_y) of slot q of
+// plane p - e_z: one box of kFdTy + 2 rows starting at row y0 - 1 - e_y and
+// BW = kFdTx + 2V columns starting at x0 - V (16 bytes before the tile, the
+// TMA start alignment; V = 16 / sizeof(T) >= 2 covers e_x = +-1 and the ring).
+// 27 boxes = one stage; ring node (lx, ly) reads element (ly, lx - 1 + V - e_x)
+// of box q, so the consumers form the ring densities and load their own node's
+// populations at compile-time offsets from shared memory.
+//
+// Per iteration p (consumer warps, 128 threads):
+//   wait full[stage p] -> rho(p) on tile + ring (sum in q order, as k_density)
+//   -> barrier -> collide plane p - 1 with the populations held in registers
+//   since the previous iteration and the gradient from the density ring ->
+//   load the own node's 27 populations of plane p from the stage -> release it.
+// The producer warp (one elected lane) refills a stage as soon as it is
+// released, so the next plane's 27 boxes land while the current plane is
+// collided.  Two stages: one being read, one in flight.
+//
+// Across a periodic x face (nx a multiple of kFdTx, >= 2 tiles) the two seam
+// tiles are staged too: the box's V columns beyond the row (zero-filled by the
+// TMA unit) are the other end of the row, which the producer loads as 27 extra
+// V-column "wrap" boxes into a side area (a TMA destination must be 128-byte
+// aligned, so they cannot land inside the box rows); the consumers copy them
+// into place (then a proxy fence, as the stage is refilled by the TMA unit
+// later) before forming the densities.  Tiles whose ring or pull sources leave
+// the plane otherwise (y0 < 2 or y0 + kFdTy + 2 > ny: the periodic y seam or a
+// wall; an x wall; a partial tile) run the LDG body of the fused kernel
+// instead (CTA-uniform).  z faces must be periodic or ghost planes (the
+// host selects this kernel only then); planes next to a ghost face take their
+// density from the exchanged field, as ring_rho.  Identical arithmetic and
+// source values as collide_stream_fd_fused, so the results are bitwise those of
+// k_collide_stream_fd.
+template <typename T> struct TmaFdLayout {
+  static constexpr int V = 16 / int(sizeof(T));
+  static constexpr int BW = kFdTx + 2 * V;  // box columns
+  static constexpr int BH = kFdTy + 2;      // box rows
+  static constexpr int kBox = ((BW * BH * int(sizeof(T)) + 127) / 128) * 128;
+  static constexpr int kWrapBox = ((V * BH * int(sizeof(T)) + 127) / 128) * 128;  // V columns x BH rows
+  static constexpr int kStages = LBM_FD_TMA_STAGES;
+  static constexpr int kOffWrap = 27 * kBox;
+  static constexpr int kStage = kOffWrap + 27 * kWrapBox;
+  static constexpr unsigned kTx = 27u * BW * BH * unsigned(sizeof(T));         // TMA bytes per stage
+  static constexpr unsigned kTxWrap = 27u * V * BH * unsigned(sizeof(T));      // + the wrap boxes (seam tile)
+  static constexpr int kOffBar = kStages * kStage;
+  static constexpr int kOffRho = kOffBar + 2 * kStages * 8;
+  static constexpr size_t kSmem = size_t(kOffRho) + sizeof(double) * 4 * (kFdTy + 2) * kFdRw;
+};
+constexpr int kFdTmaThreads = kFdThreads + 32;  // + the producer warp
+struct FdTmaMaps {
+  CUtensorMap box;   // kFdTx + 2V columns x kFdTy + 2 rows x 1 slot
+  CUtensorMap wrap;  // V columns x kFdTy + 2 rows x 1 slot (x seam)
+};
+
+template <typename T, int KIND>
+__global__ void __launch_bounds__(kFdTmaThreads, sizeof(T) == 8 ? LBM_FD_TMA_MINB64 : LBM_FD_TMA_MINB32)
+    k_collide_stream_fd_tma(const __grid_constant__ FdTmaMaps maps, const T* __restrict__ src, T* __restrict__ dst,
+                            const double* __restrict__ rf, const __grid_constant__ Consts c, int zbeg, int zstride,
+                            int zlen, int zend) {
+  using L = TmaFdLayout<T>;
+  constexpr int V = L::V;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(smem_raw + L::kOffBar);
+  unsigned long long* empty = full + L::kStages;
+  FdRho* srho = reinterpret_cast<FdRho*>(smem_raw + L::kOffRho);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int x0 = blockIdx.x * kFdTx, y0 = blockIdx.y * kFdTy;
+  auto consumer_sync = [] { asm volatile("bar.sync 1, %0;" ::"n"(kFdThreads) : "memory"); };
+  // tile whose ring and pull sources stay inside the plane (no seam, no wall)
+  const bool xseam_ok = c.face[0] == FK_WRAP && c.nx % kFdTx == 0 && c.nx >= 2 * kFdTx;
+  const bool lo_seam = xseam_ok && x0 == 0;                // box columns [0, V): x = nx - V .. nx - 1
+  const bool hi_seam = xseam_ok && x0 + kFdTx == c.nx;     // box columns [BW - V, BW): x = 0 .. V - 1
+  const bool staged = (lo_seam || hi_seam || (x0 >= kFdTx && x0 + kFdTx + 2 <= c.nx)) && y0 >= 2 &&
+                      y0 + kFdTy + 2 <= c.ny;
+  const bool seam = lo_seam || hi_seam;
+  if (!staged) {
+    if (warp < kFdThreads / 32)
+      collide_stream_fd_fused<T, KIND>(src, dst, rf, c, zbeg, zstride, zlen, zend, srho, consumer_sync,
+                                       int(threadIdx.x));
+    return;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < L::kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kFdThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int z0 = zbeg + blockIdx.z * zstride;
+  const int z1 = min(z0 + zlen, zend);
+  const int niter = z1 - z0 + 2;  // p = z0 - 1 .. z1
+  // planes whose density comes from the exchanged field (next to / beyond a ghost face)
+  auto from_field = [&](int p) {
+    return (p <= 0 && c.face[4] == FK_GHOST) || (p >= c.nzl - 1 && c.face[5] == FK_GHOST);
+  };
+
+  if (warp == kFdThreads / 32) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.box) : "memory");
+      for (int it = 0; it < niter; ++it) {
+        const int s = it % L::kStages;
+        const unsigned n = unsigned(it / L::kStages);
+        if (n > 0) mbar_wait(&empty[s], (n - 1) & 1);
+        const int p = z0 - 1 + it;
+        if (from_field(p)) {
+          mbar_arrive(&full[s]);  // nothing to stage: complete the phase
+          continue;
+        }
+        const int pw = (p < 0) ? p + c.nzl : (p >= c.nzl ? p - c.nzl : p);  // periodic z
+        mbar_expect_tx(&full[s], L::kTx + (seam ? L::kTxWrap : 0u));
+        unsigned char* sb = smem_raw + size_t(s) * L::kStage;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          int ps = pw - (k - 1);  // source plane of e_z = k - 1
+          if (ps < 0) ps += c.nzl;
+          if (ps >= c.nzl) ps -= c.nzl;
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+              const int q = LBM_Q(i, j, k);
+              tma_load_3d(sb + q * L::kBox, &maps.box, &full[s], x0 - V, y0 - j, (ps + 1) * 27 + q);
+              if (seam)
+                tma_load_3d(sb + L::kOffWrap + q * L::kWrapBox, &maps.wrap, &full[s], lo_seam ? c.nx - V : 0,
+                            y0 - j, (ps + 1) * 27 + q);
+            }
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int tid = threadIdx.x;
+  const int tx = tid % kFdTx, ty = tid / kFdTx;
+  const int x = x0 + tx, y = y0 + ty;
+  double f[27];
+  for (int it = 0; it < niter; ++it) {
+    const int s = it % L::kStages;
+    const int p = z0 - 1 + it;
+    mbar_wait(&full[s], unsigned(it / L::kStages) & 1);
+    const T* sb = reinterpret_cast<const T*>(smem_raw + size_t(s) * L::kStage);
+    constexpr int kBoxE = L::kBox / int(sizeof(T));
+    if (from_field(p)) {
+      for (int pos = tid; pos < kFdRing; pos += kFdThreads) {
+        const int ly = pos / kFdRw, lx = pos - ly * kFdRw;
+        int gx = x0 + lx - 1;  // wrapped across the periodic x seam
+        gx += (gx < 0) ? c.nx : (gx >= c.nx ? -c.nx : 0);
+        srho[p & 3][ly][lx] = __ldg(rf + (long long)(p + 1) * c.nxy + (y0 + ly - 1) * c.nx + gx);
+      }
+    } else {
+      if (seam) {  // the wrap columns into the box rows (CTA-uniform)
+        T* sbw = const_cast<T*>(sb);
+        const T* wb = reinterpret_cast<const T*>(smem_raw + size_t(s) * L::kStage + L::kOffWrap);
+        for (int i = tid; i < 27 * L::BH * V; i += kFdThreads) {
+          const int q = i / (L::BH * V), r = (i / V) % L::BH, cc = i % V;
+          sbw[q * kBoxE + r * L::BW + (lo_seam ? cc : L::BW - V + cc)] = wb[q * (L::kWrapBox / int(sizeof(T))) + r * V + cc];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the next TMA refill
+        consumer_sync();
+      }
+      for (int pos = tid; pos < kFdRing; pos += kFdThreads) {
+        const int ly = pos / kFdRw, lx = pos - ly * kFdRw;
+        const T* e = sb + ly * L::BW + lx - 1 + V;
+        double r0 = 0.0;
+#pragma unroll
+        for (int q = 0; q < 27; ++q) r0 += (double)e[q * kBoxE - (q % 3 - 1)];
+        srho[p & 3][ly][lx] = r0;
+      }
+    }
+    consumer_sync();
+    if (it >= 2) {  // collide plane p - 1 (its populations are in f since the last iteration)
+      const int z = p - 1;
+      double gxr, gyr, gzr;
+      auto at = [&](int i, int j, int k) { return srho[(z + k - 1) & 3][ty + j][tx + i]; };
+      density_gradient_g<decltype(at), true>(c, x, y, z, at, gxr, gyr, gzr);
+      StoreOwn<T> st{dst, dst + (long long)(z + 1) * c.plane + (y * c.nx + x), c.nxy, &c};
+      run_core<KIND, true>(c, f, gxr, gyr, gzr, st);
+    }
+    if (p >= z0 && p < z1) {  // own populations of plane p, collided next iteration
+      const T* e = sb + (ty + 1) * L::BW + tx + V;
+#pragma unroll
+      for (int q = 0; q < 27; ++q) f[q] = (double)e[q * kBoxE - (q % 3 - 1)];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 

@@ -104,6 +104,8 @@ struct lbm_cuboid {
   bool shape_spec = false;   // plane shape compiled in (k_collide_stream_paper_shape); env LBM_SHAPE_SPEC=0 disables
   bool tma = false;          // TMA-staged collide-stream kernel (cm_tma.cuh); opt-in LBM_TMA=1
   lbm::TmaMaps tmaps[2];     // buf[i] as the 3D tensor (x, y, 27 (nz_l + 2)) for the TMA unit
+  bool fd_tma = false;       // FULL_FD: TMA-staged fused kernel (cm_tma.cuh, k_collide_stream_fd_tma)
+  lbm::FdTmaMaps fdmaps[2];  // its tile + ring boxes (and x-seam wrap boxes) of buf[i]
   int tma_grid = 0;          // persistent grid size of the TMA kernel (resident CTAs)
   bool xpair = false;        // fp32 storage, nx even: x-pair kernel (float2 loads/stores); opt-in LBM_XPAIR=1
   bool aa = false;           // AA in-place streaming: one buffer; cur = 0 layout R, cur = 1 layout N
@@ -437,8 +439,15 @@ int launch_cs(lbm_cuboid* h, const void* src, void* dst, int zbeg, int nplanes, 
     const dim3 gf(unsigned((h->p.nx + lbm::kFdTx - 1) / lbm::kFdTx), unsigned((h->p.ny + lbm::kFdTy - 1) / lbm::kFdTy),
                   unsigned(nchunks));
     const int kind = (h->p.model == LBM_MODEL_RM) ? lbm::CORE_RAW : (h->paper_rates ? lbm::CORE_PAPER : lbm::CORE_GENERIC);
-#define LBM_FDF(T, K) \
-  lbm::k_collide_stream_fd<T, K><<<gf, lbm::kFdThreads, 0, s>>>((const T*)src, (T*)dst, rf, cc, zbeg, zst, zlen, zend)
+#define LBM_FDF(T, K)                                                                                          \
+  do {                                                                                                         \
+    if (h->fd_tma && zstride == 1)                                                                             \
+      lbm::k_collide_stream_fd_tma<T, K><<<gf, lbm::kFdTmaThreads, lbm::TmaFdLayout<T>::kSmem, s>>>(           \
+          h->fdmaps[(src == h->buf[0]) ? 0 : 1], (const T*)src, (T*)dst, rf, cc, zbeg, zst, zlen, zend);       \
+    else                                                                                                       \
+      lbm::k_collide_stream_fd<T, K><<<gf, lbm::kFdThreads, 0, s>>>((const T*)src, (T*)dst, rf, cc, zbeg, zst, \
+                                                                    zlen, zend);                               \
+  } while (0)
     if (fp64) {
       if (kind == lbm::CORE_PAPER) LBM_FDF(double, lbm::CORE_PAPER);
       else if (kind == lbm::CORE_RAW) LBM_FDF(double, lbm::CORE_RAW);
@@ -656,6 +665,52 @@ int tma_setup(lbm_cuboid* h) {
          : kind == CORE_RAW ? (const void*)k_collide_stream_tma<float, CORE_RAW>
                             : (const void*)k_collide_stream_tma<float, CORE_GENERIC>;
   return fp64 ? tma_kernel_setup<double>(h, fn) : tma_kernel_setup<float>(h, fn);
+}
+
+// FULL_FD TMA kernel: one tensor map per buffer (box kFdTx + 2V columns x
+// kFdTy + 2 rows x 1 slot), shared-memory opt-in of the instantiation in use
+int fd_tma_setup(lbm_cuboid* h) {
+  PfnEncodeTiled enc = nullptr;
+  int rc;
+  if ((rc = driver_fn("cuTensorMapEncodeTiled", &enc))) return rc;
+  const bool fp64 = (h->p.precision == LBM_FP64);
+  const cuuint64_t e = fp64 ? 8 : 4;
+  const cuuint64_t dims[3] = {cuuint64_t(h->p.nx), cuuint64_t(h->p.ny), cuuint64_t(27) * cuuint64_t(h->nzl + 2)};
+  const cuuint64_t strides[2] = {cuuint64_t(h->p.nx) * e, cuuint64_t(h->nxy) * e};
+  const cuuint32_t V = cuuint32_t(16 / e);
+  const cuuint32_t boxes[2][3] = {{cuuint32_t(lbm::kFdTx) + 2 * V, cuuint32_t(lbm::kFdTy + 2), 1},
+                                  {V, cuuint32_t(lbm::kFdTy + 2), 1}};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  for (int i = 0; i < 2; ++i) {
+    CUtensorMap* maps[2] = {&h->fdmaps[i].box, &h->fdmaps[i].wrap};
+    for (int w = 0; w < 2; ++w) {
+      CUresult r = enc(maps[w], fp64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                       h->buf[i], dims, strides, boxes[w], estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) return fail(LBM_ECUDA, "cuTensorMapEncodeTiled failed (%d)", int(r));
+    }
+  }
+  using namespace lbm;
+  const int kind = (h->p.model == LBM_MODEL_RM) ? CORE_RAW : (h->paper_rates ? CORE_PAPER : CORE_GENERIC);
+  const void* fn;
+  int smem;
+  if (fp64) {
+    fn = kind == CORE_PAPER ? (const void*)k_collide_stream_fd_tma<double, CORE_PAPER>
+         : kind == CORE_RAW ? (const void*)k_collide_stream_fd_tma<double, CORE_RAW>
+                            : (const void*)k_collide_stream_fd_tma<double, CORE_GENERIC>;
+    smem = int(TmaFdLayout<double>::kSmem);
+  } else {
+    fn = kind == CORE_PAPER ? (const void*)k_collide_stream_fd_tma<float, CORE_PAPER>
+         : kind == CORE_RAW ? (const void*)k_collide_stream_fd_tma<float, CORE_RAW>
+                            : (const void*)k_collide_stream_fd_tma<float, CORE_GENERIC>;
+    smem = int(TmaFdLayout<float>::kSmem);
+  }
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int per_sm = 0;
+  CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFdTmaThreads, smem));
+  if (per_sm < 1) return fail(LBM_ECUDA, "FULL_FD TMA kernel cannot be resident");
+  return LBM_OK;
 }
 
 void drop_graphs(lbm_cuboid* h) {
@@ -1241,6 +1296,17 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
     h->tma = tma_env && std::atoi(tma_env) != 0 && !h->aa && !h->fd && (size_t(p->nx) * h->elem) % 16 == 0 &&
              p->nx >= lbm::kTmaTx && (align % 16) == 0;
     if (h->tma && (rc = tma_setup(h))) return bail(rc);
+    // FULL_FD (same-time density) with the TMA-staged fused kernel (LBM_FD_TMA=1):
+    // z faces periodic or ghost planes (the kernel has no z-wall rules), not
+    // the P2P halo (whose interior must not touch the ghost planes)
+    const char* fdt = std::getenv("LBM_FD_TMA");
+    const auto zok = [](int fk) { return fk == lbm::FK_WRAP || fk == lbm::FK_GHOST; };
+    h->fd_tma = fdt && std::atoi(fdt) != 0 && h->fd && !h->fd_lag && !h->aa && !h->p2p && zok(h->c.face[4]) &&
+                zok(h->c.face[5]) && (size_t(p->nx) * h->elem) % 16 == 0 && (align % 16) == 0;
+    if (h->fd_tma) {
+      h->fd_fused = true;
+      if ((rc = fd_tma_setup(h))) return bail(rc);
+    }
   }
   if (p->check_every > 0 &&
       (cudaHostAlloc(&h->h_watch, 8 * sizeof(double), cudaHostAllocDefault) != cudaSuccess ||
@@ -1602,7 +1668,7 @@ const char* lbm_cuboid_kernel_name(const lbm_cuboid_t* h) {
             ? std::string("k_aa_shape<") + t + "," + std::to_string(h->p.nx) + "," + std::to_string(h->p.ny) + ">"
             : std::string("k_aa<") + t + ">";
   } else if (h->fd && h->fd_fused && !h->p2p) {
-    k = std::string("k_collide_stream_fd<") + t + ">";
+    k = std::string(h->fd_tma ? "k_collide_stream_fd_tma<" : "k_collide_stream_fd<") + t + ">";
   } else if (h->tma && !h->fd) {
     k = std::string("k_collide_stream_tma<") + t + ">";
   } else if (h->xpair && h->p.precision != LBM_FP64 && !h->fd) {
