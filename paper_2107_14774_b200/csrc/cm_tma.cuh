@@ -62,7 +62,7 @@ namespace lbm {
 #define LBM_FD_TMA_MINB64 2  // resident CTAs per SM (fp64: 2 x 103 KB of shared memory)
 #endif
 #ifndef LBM_FD_TMA_MINB32
-#define LBM_FD_TMA_MINB32 2
+#define LBM_FD_TMA_MINB32 3
 #endif
 #ifndef LBM_TMA_WRAPBOX32
 #define LBM_TMA_WRAPBOX32 1  // fp32: stage the x-wrap column with wrap boxes

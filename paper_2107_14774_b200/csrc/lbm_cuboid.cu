@@ -667,6 +667,23 @@ int tma_setup(lbm_cuboid* h) {
   return fp64 ? tma_kernel_setup<double>(h, fn) : tma_kernel_setup<float>(h, fn);
 }
 
+// Fraction of the FULL_FD tiles (kFdTx x kFdTy) that the TMA kernel stages
+// (the predicate of k_collide_stream_fd_tma)
+double fd_tma_staged_fraction(int nx, int ny, bool xper) {
+  const int ntx = (nx + lbm::kFdTx - 1) / lbm::kFdTx, nty = (ny + lbm::kFdTy - 1) / lbm::kFdTy;
+  const bool seam_ok = xper && nx % lbm::kFdTx == 0 && nx >= 2 * lbm::kFdTx;
+  int sx = 0, sy = 0;
+  for (int b = 0; b < ntx; ++b) {
+    const int x0 = b * lbm::kFdTx;
+    sx += (seam_ok && (x0 == 0 || x0 + lbm::kFdTx == nx)) || (x0 >= lbm::kFdTx && x0 + lbm::kFdTx + 2 <= nx);
+  }
+  for (int b = 0; b < nty; ++b) {
+    const int y0 = b * lbm::kFdTy;
+    sy += y0 >= 2 && y0 + lbm::kFdTy + 2 <= ny;
+  }
+  return double(sx) * double(sy) / (double(ntx) * double(nty));
+}
+
 // FULL_FD TMA kernel: one tensor map per buffer (box kFdTx + 2V columns x
 // kFdTy + 2 rows x 1 slot), shared-memory opt-in of the instantiation in use
 int fd_tma_setup(lbm_cuboid* h) {
@@ -707,6 +724,8 @@ int fd_tma_setup(lbm_cuboid* h) {
     smem = int(TmaFdLayout<float>::kSmem);
   }
   CU(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  // all of the unified L1 / shared memory as shared memory (2-3 CTAs per SM)
+  CU(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, int(cudaSharedmemCarveoutMaxShared)));
   int per_sm = 0;
   CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kFdTmaThreads, smem));
   if (per_sm < 1) return fail(LBM_ECUDA, "FULL_FD TMA kernel cannot be resident");
@@ -1296,13 +1315,18 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
     h->tma = tma_env && std::atoi(tma_env) != 0 && !h->aa && !h->fd && (size_t(p->nx) * h->elem) % 16 == 0 &&
              p->nx >= lbm::kTmaTx && (align % 16) == 0;
     if (h->tma && (rc = tma_setup(h))) return bail(rc);
-    // FULL_FD (same-time density) with the TMA-staged fused kernel (LBM_FD_TMA=1):
-    // z faces periodic or ghost planes (the kernel has no z-wall rules), not
-    // the P2P halo (whose interior must not touch the ghost planes)
-    const char* fdt = std::getenv("LBM_FD_TMA");
+    // FULL_FD (same-time density): the TMA-staged fused kernel where it applies
+    // -- z faces periodic or ghost planes (it has no z-wall rules; its interior
+    // never reads a ghost plane, so the P2P halo may use it too), rows of a
+    // 16-byte multiple -- by default when >= 3/4 of its tiles are staged (the
+    // rest run the LDG body, slower than the two-pass path);
+    // LBM_FD_TMA=0/1 forces it off / on
     const auto zok = [](int fk) { return fk == lbm::FK_WRAP || fk == lbm::FK_GHOST; };
-    h->fd_tma = fdt && std::atoi(fdt) != 0 && h->fd && !h->fd_lag && !h->aa && !h->p2p && zok(h->c.face[4]) &&
-                zok(h->c.face[5]) && (size_t(p->nx) * h->elem) % 16 == 0 && (align % 16) == 0;
+    const bool fdt_ok = h->fd && !h->fd_lag && !h->aa && zok(h->c.face[4]) && zok(h->c.face[5]) &&
+                        (size_t(p->nx) * h->elem) % 16 == 0 && (align % 16) == 0;
+    bool fdt_on = fdt_ok && fd_tma_staged_fraction(p->nx, p->ny, h->c.face[0] == lbm::FK_WRAP) >= 0.75;
+    if (const char* e = std::getenv("LBM_FD_TMA")) fdt_on = fdt_ok && std::atoi(e) != 0;
+    h->fd_tma = fdt_on;
     if (h->fd_tma) {
       h->fd_fused = true;
       if ((rc = fd_tma_setup(h))) return bail(rc);
@@ -1667,7 +1691,7 @@ const char* lbm_cuboid_kernel_name(const lbm_cuboid_t* h) {
     k = (h->shape_spec && h->paper_rates && h->p.model == LBM_MODEL_CM)
             ? std::string("k_aa_shape<") + t + "," + std::to_string(h->p.nx) + "," + std::to_string(h->p.ny) + ">"
             : std::string("k_aa<") + t + ">";
-  } else if (h->fd && h->fd_fused && !h->p2p) {
+  } else if (h->fd && h->fd_fused) {  // (the P2P interior launch too)
     k = std::string(h->fd_tma ? "k_collide_stream_fd_tma<" : "k_collide_stream_fd<") + t + ">";
   } else if (h->tma && !h->fd) {
     k = std::string("k_collide_stream_tma<") + t + ">";

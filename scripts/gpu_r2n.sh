@@ -2,7 +2,7 @@
 # the reports are summarised to CSV on the box (the .ncu-rep files exceed the copy-back limit)
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/prof_r2
-NCU="ncu --set full --clock-control none --import-source on -k regex:k_collide_stream -s 1 -c 1"
+NCU="ncu -f --set full --clock-control none --import-source on -k regex:k_collide_stream -s 1 -c 1"
 run() {  # name, env..., args
   n=$1; shift
   env "$@" python scripts/prof_one.py $ARGS > gpurun_out/prof_r2/$n.plain.log 2>&1 && \

@@ -4,8 +4,8 @@ import os
 import re
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-DOCS = ["DESIGN.md", "README.md", "profiles/r1/SUMMARY.md", "scripts/README.md"]
-SEARCH = ["", "profiles/r1", "profiles", "scripts", "tests", "results", "paper_2107_14774_b200",
+DOCS = ["DESIGN.md", "README.md", "profiles/r1/SUMMARY.md", "profiles/r2/SUMMARY.md", "scripts/README.md"]
+SEARCH = ["", "profiles/r1", "profiles/r2", "profiles", "scripts", "tests", "results", "paper_2107_14774_b200",
           "paper_2107_14774_b200/csrc", "studies", "examples", "include", "oracle"]
 EXTERNAL = {"SPEC.md", "PAPER.md"}  # the reference (not in this repository)
 PAT = re.compile(r"`([A-Za-z0-9_./{},\-]+\.(?:py|cu|cuh|h|c|sh|json|jsonl|csv|md|ncu-rep))`")

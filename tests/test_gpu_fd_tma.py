@@ -10,8 +10,9 @@ reading R16) on the B200:
 * against the LDG fused kernel (LBM_FD_FUSED=1) on the same inputs: the two
   inline the same per-node arithmetic on the same source values (max|df| <=
   1e-14 fp64, relative <= 1e-6 fp32; equal unless ptxas contracts a
-  multiply-add differently), through the NCCL ghost-plane path too (interior
-  launch staged, boundary planes from the exchanged density field);
+  multiply-add differently), through the NCCL ghost-plane path and the fused
+  P2P halo too (interior launch staged, the density of the planes next to the
+  ghost faces from the density field);
 * geometries: periodic (seam tiles on the LDG body), free-slip y walls, x and y
   bounce-back walls with the moving lid and periodic z, generic rates and body
   force, the raw-moment model; z walls select the LDG kernel (kernel_name).
@@ -95,6 +96,9 @@ def test_fd_tma_matches_ldg_fused(P, case, prec, monkeypatch):
     hs = [_lattice(P, monkeypatch, w, {}, True, graphs=1), _lattice(P, monkeypatch, w, {}, True, graphs=2)]
     if w.bc[4] == synth.BC_PERIODIC:
         hs.append(_lattice(P, monkeypatch, w, {}, True, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id()))
+        hs.append(_lattice(P, monkeypatch, w, {}, True, halo=P.HALO_P2P))  # the slab is its own neighbour
+    for g in hs:
+        assert "fd_tma" in g.kernel_name()
     for g in [a] + hs:
         g.init_fields(rho, u)
         g.step(23)
@@ -116,6 +120,17 @@ def test_fd_tma_not_selected_with_z_walls(P, monkeypatch):
     name = g.kernel_name()
     g.close()
     assert "fd_tma" not in name and "k_collide_stream_fd" in name
+
+
+def test_fd_tma_default_selection(P):
+    """Default (no LBM_FD_TMA): the TMA kernel where >= 3/4 of the tiles are
+    staged (the bench's 512 x 512 planes), the two-pass path otherwise."""
+    for (nx, ny, on) in [(512, 512, True), (160, 36, True), (64, 16, False), (40, 24, False), (196, 30, False)]:
+        w = synth.CONFIGS["tgv"].scaled(nx=nx, ny=ny, nz=4, corrections=FD)
+        g = P.Lattice(**w.params())
+        name = g.kernel_name()
+        g.close()
+        assert ("fd_tma" in name) == on, (nx, ny, name)
 
 
 def test_fd_tma_bench_geometry_sampled_oracle(P, monkeypatch):

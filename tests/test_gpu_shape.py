@@ -81,8 +81,11 @@ def test_kernel_name_reports_the_launched_variant(P, monkeypatch):
     g = P.Lattice(**w.scaled(nx=96, ny=40, precision=1).params())
     assert g.kernel_name() == "k_collide_stream_paper<float>"
     g.close()
-    g = P.Lattice(**w.scaled(nx=96, ny=40, corrections=synth.CORR_FULL_FD).params())
+    g = P.Lattice(**w.scaled(nx=40, ny=40, corrections=synth.CORR_FULL_FD).params())
     assert g.kernel_name() == "k_collide_stream_paper<double> + k_density"
+    g.close()
+    g = P.Lattice(**w.scaled(nx=96, ny=40, corrections=synth.CORR_FULL_FD).params())
+    assert g.kernel_name() == "k_collide_stream_fd_tma<double>"  # 9 of 10 tile rows staged
     g.close()
     monkeypatch.setenv("LBM_SHAPE_SPEC", "0")
     g = P.Lattice(**w.scaled(model=1).params())
