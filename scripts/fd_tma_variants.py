@@ -14,10 +14,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
 VARIANTS = {
-    "rho2": [],
-    "rho1": ["LBM_FD_TMA_RHO2=0"],
-    "rho2_zc48": ["LBM_FD_ZC=48"],
-    "rho2_m32_2": ["LBM_FD_TMA_MINB32=2"],
+    "rhowarp": [],
+    "consumer_rho": ["LBM_FD_TMA_RHOWARP=0"],
+    "rhowarp_m32_2": ["LBM_FD_TMA_MINB32=2"],
+    "rhowarp_zc64": ["LBM_FD_ZC=64"],
 }
 
 if sys.argv[1] == "build":
