@@ -384,6 +384,13 @@ __global__ void __launch_bounds__(kFdTmaThreads, sizeof(T) == 8 ? LBM_FD_TMA_MIN
   const int z1 = min(z0 + zlen, zend);
   const int niter = z1 - z0 + 2;  // p = z0 - 1 .. z1
   // planes whose density comes from the exchanged field (next to / beyond a ghost face)
+  // a plane is staged when its density is summed here or its populations are
+  // collided in this launch (a plane next to a ghost face collided by a
+  // contiguous boundary launch, nz_l = 2: density from the field, populations staged)
+  auto staged_plane = [&](int p) {
+    return !((p <= 0 && c.face[4] == FK_GHOST) || (p >= c.nzl - 1 && c.face[5] == FK_GHOST)) ||
+           (p >= z0 && p < z1);
+  };
   auto from_field = [&](int p) {
     return (p <= 0 && c.face[4] == FK_GHOST) || (p >= c.nzl - 1 && c.face[5] == FK_GHOST);
   };
@@ -397,18 +404,19 @@ __global__ void __launch_bounds__(kFdTmaThreads, sizeof(T) == 8 ? LBM_FD_TMA_MIN
         const unsigned n = unsigned(it / L::kStages);
         if (n > 0) mbar_wait(&empty[s], (n - 1) & 1);
         const int p = z0 - 1 + it;
-        if (from_field(p)) {
+        if (!staged_plane(p)) {
           mbar_arrive(&full[s]);  // nothing to stage: complete the phase
           continue;
         }
-        const int pw = (p < 0) ? p + c.nzl : (p >= c.nzl ? p - c.nzl : p);  // periodic z
+        // periodic z (a plane beyond a ghost face is never staged)
+        const int pw = (p < 0) ? p + c.nzl : (p >= c.nzl ? p - c.nzl : p);
         mbar_expect_tx(&full[s], L::kTx + (seam ? L::kTxWrap : 0u));
         unsigned char* sb = smem_raw + size_t(s) * L::kStage;
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          int ps = pw - (k - 1);  // source plane of e_z = k - 1
-          if (ps < 0) ps += c.nzl;
-          if (ps >= c.nzl) ps -= c.nzl;
+          int ps = pw - (k - 1);  // source plane of e_z = k - 1: wrapped, or the ghost plane -1 / nz_l
+          if (ps < 0 && c.face[4] == FK_WRAP) ps += c.nzl;
+          if (ps >= c.nzl && c.face[5] == FK_WRAP) ps -= c.nzl;
 #pragma unroll
           for (int j = 0; j < 3; ++j)
 #pragma unroll
@@ -436,6 +444,16 @@ __global__ void __launch_bounds__(kFdTmaThreads, sizeof(T) == 8 ? LBM_FD_TMA_MIN
     mbar_wait(&full[s], unsigned(it / L::kStages) & 1);
     const T* sb = reinterpret_cast<const T*>(smem_raw + size_t(s) * L::kStage);
     constexpr int kBoxE = L::kBox / int(sizeof(T));
+    if (seam && staged_plane(p)) {  // the wrap columns into the box rows (CTA-uniform)
+      T* sbw = const_cast<T*>(sb);
+      const T* wb = reinterpret_cast<const T*>(smem_raw + size_t(s) * L::kStage + L::kOffWrap);
+      for (int i = tid; i < 27 * L::BH * V; i += kFdThreads) {
+        const int q = i / (L::BH * V), r = (i / V) % L::BH, cc = i % V;
+        sbw[q * kBoxE + r * L::BW + (lo_seam ? cc : L::BW - V + cc)] = wb[q * (L::kWrapBox / int(sizeof(T))) + r * V + cc];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the next TMA refill
+      consumer_sync();
+    }
     if (from_field(p)) {
       for (int pos = tid; pos < kFdRing; pos += kFdThreads) {
         const int ly = pos / kFdRw, lx = pos - ly * kFdRw;
@@ -444,16 +462,6 @@ __global__ void __launch_bounds__(kFdTmaThreads, sizeof(T) == 8 ? LBM_FD_TMA_MIN
         srho[p & 3][ly][lx] = __ldg(rf + (long long)(p + 1) * c.nxy + (y0 + ly - 1) * c.nx + gx);
       }
     } else {
-      if (seam) {  // the wrap columns into the box rows (CTA-uniform)
-        T* sbw = const_cast<T*>(sb);
-        const T* wb = reinterpret_cast<const T*>(smem_raw + size_t(s) * L::kStage + L::kOffWrap);
-        for (int i = tid; i < 27 * L::BH * V; i += kFdThreads) {
-          const int q = i / (L::BH * V), r = (i / V) % L::BH, cc = i % V;
-          sbw[q * kBoxE + r * L::BW + (lo_seam ? cc : L::BW - V + cc)] = wb[q * (L::kWrapBox / int(sizeof(T))) + r * V + cc];
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes before the next TMA refill
-        consumer_sync();
-      }
       for (int pos = tid; pos < kFdRing; pos += kFdThreads) {
         const int ly = pos / kFdRw, lx = pos - ly * kFdRw;
         const T* e = sb + ly * L::BW + lx - 1 + V;

@@ -47,6 +47,10 @@ CASES = {
     "walls_xy_lid_zper": (synth.CONFIGS["cavity100"].scaled(nx=136, ny=22, nz=9, bc=(BB, BB, BB, MW, P_, P_)), {}),
     "generic_force": (synth.CONFIGS["tgv"].scaled(nx=128, ny=20, nz=8),
                       {"omega_1": 1.2, "omega_high": 0.9, "force": (1e-5, -2e-6, 3e-6)}),
+    # one- and two-plane slabs: with ghost planes the boundary launch is contiguous
+    # and collides planes whose density comes from the exchanged field
+    "tgv_nz2": (synth.CONFIGS["tgv"].scaled(nx=96, ny=20, nz=2), {}),
+    "tgv_nz1": (synth.CONFIGS["tgv"].scaled(nx=64, ny=16, nz=1), {}),
 }
 
 

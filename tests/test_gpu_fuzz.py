@@ -239,3 +239,71 @@ def test_random_problem_p2p_slabs_match_oracle(P, i):
         pytest.skip("unstable draw: the oracle's state blows up (S:L407 criterion or 4x growth)")
     spread = _fp32_spread(kw, f0, steps) if kw["precision"] == 1 else 0.0
     _assert_close(fg, fo, kw["precision"], (kw, world), spread)
+
+
+N_FDTMA_CASES = int(os.environ.get("LBM_FUZZ_FDTMA_CASES", "30"))
+
+
+def _fdtma_cases():
+    """Random FULL_FD problem statements on planes where the TMA-staged fused
+    kernel stages most tiles (nx a multiple of 32 >= 64 or wider with x walls,
+    ny >= 12), z periodic (its domain), any x / y boundary kinds, either model,
+    rates, force, precision, launch and halo mode."""
+    rng = np.random.Generator(np.random.PCG64(1474))
+    out = []
+    while len(out) < N_FDTMA_CASES:
+        kw, gpu = _draw(rng)
+        kw["corrections"] = synth.CORR_FULL_FD
+        kw["nx"] = int(rng.choice([64, 96, 128, 100, 72]))  # rows of a 16-byte multiple in fp32 too
+        kw["ny"] = int(rng.integers(12, 31))
+        kw["nz"] = int(rng.integers(2, 8))
+        kw["bc"] = tuple(kw["bc"][:4]) + (PER, PER)
+        gpu = dict(graphs=int(rng.integers(0, 3)))
+        roll = rng.random()
+        if roll < 0.2:
+            gpu["halo"] = 2
+        elif roll < 0.4:
+            gpu["halo"] = 1
+        out.append((kw, gpu))
+    return out
+
+
+FDTMA_CASES = _fdtma_cases()
+
+
+@pytest.mark.parametrize("i", range(N_FDTMA_CASES))
+def test_random_fd_problem_tma_kernel_matches_oracle(P, i, monkeypatch):
+    """FULL_FD through the TMA-staged fused kernel (LBM_FD_TMA=1) on random
+    problem statements against the oracle, 13 steps (bars as above)."""
+    import oracle as O
+
+    kw, gpu = FDTMA_CASES[i]
+    if gpu.get("halo") == 1:
+        gpu = dict(gpu, nccl_uid=P.nccl_unique_id())
+    monkeypatch.setenv("LBM_FD_TMA", "1")
+    try:
+        g = P.Lattice(**kw, **gpu)
+    except P.LbmError as e:
+        assert e.code in (P.lbm.LBM_EINVAL, P.lbm.LBM_ENOTSUP), e
+        pytest.skip(f"rejected by the ABI: {e}")
+    finally:
+        monkeypatch.delenv("LBM_FD_TMA")
+    assert "fd_tma" in g.kernel_name(), g.kernel_name()
+    o = O.Oracle(**kw)
+    nx, ny, nz = kw["nx"], kw["ny"], kw["nz"]
+    rho, u = synth.random_fields(nx, ny, nz, 300 + i)
+    o.init_fields(rho, u)
+    f0 = o.get_populations() * (1.0 + 1e-3 * synth.noise((27, nz, ny, nx), 1300 + i))
+    o.set_populations(f0)
+    g.set_populations(f0)
+    steps = 13
+    o.step(steps)
+    g.step(steps)
+    g.sync()
+    fo, fg = o.get_populations(), g.get_populations()
+    g.close()
+    assert np.all(np.isfinite(fg)) or not _stable(o, f0)
+    if not _stable(o, f0):
+        pytest.skip("unstable draw: the oracle's state blows up (S:L407 criterion or 4x growth)")
+    spread = _fp32_spread(kw, f0, steps) if kw["precision"] == 1 else 0.0
+    _assert_close(fg, fo, kw["precision"], (kw, gpu), spread)
