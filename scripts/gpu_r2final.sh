@@ -13,7 +13,7 @@ python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline --precision fp32
 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv -k regex:k_collide_stream -s 3 -c 1 python bench.py --steps 3 --warmup 2 --no-e2e --no-cpu-baseline --precision fp32 > gpurun_out/final/ncu_traffic_fp32.csv 2>&1; echo "ncu32 $?"
 for prec in fp64 fp32; do
   python scripts/prof_one.py $prec > /dev/null 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:k_collide_stream -s 1 -c 1 -o /tmp/shape_$prec python scripts/prof_one.py $prec > gpurun_out/final/ncu_full_$prec.log 2>&1
+  ncu -f --set full --clock-control none --import-source on -k regex:k_collide_stream -s 1 -c 1 -o /tmp/shape_$prec python scripts/prof_one.py $prec > gpurun_out/final/ncu_full_$prec.log 2>&1
   echo "ncu full $prec $?"
   ncu -i /tmp/shape_$prec.ncu-rep --page details --csv > gpurun_out/final/shape_${prec}_details.csv 2>/dev/null
   ncu -i /tmp/shape_$prec.ncu-rep --page raw --csv > gpurun_out/final/shape_${prec}_raw.csv 2>/dev/null
