@@ -14,10 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
 VARIANTS = {
-    "rhowarp": [],
-    "consumer_rho": ["LBM_FD_TMA_RHOWARP=0"],
-    "rhowarp_m32_2": ["LBM_FD_TMA_MINB32=2"],
-    "rhowarp_zc64": ["LBM_FD_ZC=64"],
+    "base": [],
+    "s3_m32_2": ["LBM_FD_TMA_STAGES=3", "LBM_FD_TMA_MINB32=2", "LBM_FD_TMA_MINB64=1"],
 }
 
 if sys.argv[1] == "build":

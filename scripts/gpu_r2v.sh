@@ -1,4 +1,4 @@
-# ncu --set full of the FULL_FD TMA kernel (fp64, fp32) on 512x512x64, summarised to CSV on the box
+# ncu --set full of the FULL_FD TMA kernel (fp64, fp32) and the LDG fused kernel on 512x512x64, summarised to CSV on the box
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out/prof_r2
 NCU="ncu -f --set full --clock-control none --import-source on -k regex:k_collide_stream_fd -s 1 -c 1"
@@ -12,7 +12,6 @@ run() {  # name, env..., args
   ncu -i /tmp/$n.ncu-rep --page source --csv --print-source sass > /tmp/${n}_sass.csv 2>/dev/null
   gzip -c /tmp/${n}_sass.csv > gpurun_out/prof_r2/${n}_sass.csv.gz
 }
-ARGS="fp64 full_fd" run fdtma_fp64 LBM_FD_TMA=1 LBM_FD_FUSED=1
-
-
-ls -la gpurun_out/prof_r2/ | tail
+ARGS="fp64 full_fd" run fdtma_fp64 LBM_FD_TMA=1
+ARGS="fp32 full_fd" run fdtma_fp32 LBM_FD_TMA=1
+ARGS="fp64 full_fd" run fdldg_fp64 LBM_FD_TMA=0 LBM_FD_FUSED=1
