@@ -15,7 +15,9 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
 VARIANTS = {
     "base": [],
-    "s3_m32_2": ["LBM_FD_TMA_STAGES=3", "LBM_FD_TMA_MINB32=2", "LBM_FD_TMA_MINB64=1"],
+    "l2hint": ["LBM_FD_TMA_L2HINT=1"],
+    "balance": ["LBM_FD_TMA_BALANCE=1"],
+    "l2hint_balance": ["LBM_FD_TMA_L2HINT=1", "LBM_FD_TMA_BALANCE=1"],
 }
 
 if sys.argv[1] == "build":

@@ -4,7 +4,8 @@ or the -DLBM_DEBUG_BOUNDS build): init (host and device), collide-stream
 (paper-rate, generic, raw; fp64 and fp32), FULL_FD fused and two-pass, all wall
 kinds, ghost-plane NCCL self-exchange, fused P2P halo (self and two in-process
 slabs), graphs, the persistent kernel, AA, macro, pack/unpack, check; round 2:
-FULL_FD_LAG (all paths), the opt-in TMA and x-pair kernels, the event trace."""
+FULL_FD_LAG (all paths), the TMA-staged FULL_FD kernel, the opt-in TMA and
+x-pair kernels, the event trace."""
 import os
 import sys
 
@@ -101,5 +102,23 @@ for env, ws in (("LBM_TMA", [synth.CONFIGS["tgv"].scaled(nx=136, ny=5, nz=4),
             g.sync()
             g.close()
     os.environ.pop(env)
+# the TMA-staged FULL_FD kernel: staged, x-seam and LDG-body tiles, x/y walls with
+# periodic z, the NCCL ghost path and a 2-plane slab
+os.environ["LBM_FD_TMA"] = "1"
+for w, kw in ((synth.CONFIGS["tgv"].scaled(nx=96, ny=20, nz=6, corrections=3), {}),
+              (synth.CONFIGS["tgv"].scaled(nx=96, ny=20, nz=6, corrections=3), {"halo": P.HALO_NCCL}),
+              (synth.CONFIGS["tgv"].scaled(nx=64, ny=16, nz=2, corrections=3), {"halo": P.HALO_NCCL}),
+              (synth.CONFIGS["cavity100"].scaled(nx=100, ny=18, nz=5, corrections=3, bc=(1, 1, 1, 2, 0, 0)), {})):
+    for prec in (0, 1):
+        if "halo" in kw:
+            kw = dict(kw, nccl_uid=P.nccl_unique_id())
+        g = P.Lattice(**w.scaled(precision=prec).params(), **kw)
+        assert "fd_tma" in g.kernel_name(), g.kernel_name()
+        rho, u = synth.random_fields(w.nx, w.ny, w.nz, 7)
+        g.init_fields(rho, u)
+        g.step(6)
+        g.sync()
+        g.close()
+os.environ.pop("LBM_FD_TMA")
 torch.cuda.synchronize()
 print("sanitize_run: all kernels exercised")
