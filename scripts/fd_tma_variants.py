@@ -15,9 +15,8 @@ sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
 VARIANTS = {
     "base": [],
-    "l2hint": ["LBM_FD_TMA_L2HINT=1"],
-    "balance": ["LBM_FD_TMA_BALANCE=1"],
-    "l2hint_balance": ["LBM_FD_TMA_L2HINT=1", "LBM_FD_TMA_BALANCE=1"],
+    "s1_m3": ["LBM_FD_TMA_STAGES=1", "LBM_FD_TMA_MINB64=3", "LBM_FD_TMA_MINB32=4"],
+    "s1_m2": ["LBM_FD_TMA_STAGES=1", "LBM_FD_TMA_MINB64=2", "LBM_FD_TMA_MINB32=3"],
 }
 
 if sys.argv[1] == "build":
