@@ -14,9 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
 VARIANTS = {
-    "base": [],
-    "s1_m3": ["LBM_FD_TMA_STAGES=1", "LBM_FD_TMA_MINB64=3", "LBM_FD_TMA_MINB32=4"],
-    "s1_m2": ["LBM_FD_TMA_STAGES=1", "LBM_FD_TMA_MINB64=2", "LBM_FD_TMA_MINB32=3"],
+    "walls_branch": [],
+    "walls_nobranch": ["LBM_FD_TMA_GRADBRANCH=0"],
 }
 
 if sys.argv[1] == "build":
@@ -36,8 +35,10 @@ else:
     for n in only:
         for prec in ("fp64", "fp32"):
             env = dict(os.environ, LBM_CUBOID_LIB=os.path.join(VDIR, f"lib_fdtma_{n}.so"), LBM_FD_TMA="1")
+            extra = os.environ.get("FD_VARIANT_ARGS", "").split()
             r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "20", "--warmup", "3",
-                                "--corrections", "full_fd", "--precision", prec, "--no-e2e", "--no-cpu-baseline"],
+                                "--corrections", "full_fd", "--precision", prec, "--no-e2e", "--no-cpu-baseline",
+                                *extra],
                                capture_output=True, text=True, env=env, timeout=400)
             try:
                 d = json.loads(r.stdout.strip().splitlines()[-1])
