@@ -273,6 +273,10 @@ __global__ void __launch_bounds__(kTmaThreads, LBM_TMA_MINB)
         }
       }
     }
+    // release the stage: every thread's shared-memory reads of it are ordered
+    // before the TMA unit's next writes into it (async proxy) -- without the
+    // fence a warp's outstanding loads could read the refilled stage
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     if (!active) continue;
@@ -485,6 +489,10 @@ __global__ void __launch_bounds__(kFdTmaThreads, sizeof(T) == 8 ? LBM_FD_TMA_MIN
 #pragma unroll
       for (int q = 0; q < 27; ++q) f[q] = (double)e[q * kBoxE - (q % 3 - 1)];
     }
+    // release the stage: every thread's shared-memory reads of it are ordered
+    // before the TMA unit's next writes into it (async proxy) -- without the
+    // fence a warp's outstanding loads could read the refilled stage
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }

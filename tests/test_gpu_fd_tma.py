@@ -167,3 +167,24 @@ def test_fd_tma_bench_geometry_sampled_oracle(P, monkeypatch):
             sub.step(1)
             ref = sub.get_populations()[:, 2, 2, 2]
             assert np.abs(f1[:, z, y, x] - ref).max() <= 1e-13, (x, y, z)
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+def test_fd_tma_full_plane_bitwise_and_deterministic(P, prec, monkeypatch):
+    """The bench's 512 x 512 planes, 64 planes (two 32-plane chunks per tile: 34
+    pipelined planes per CTA), 12 steps: two runs of the TMA kernel are bitwise
+    equal to each other and to the LDG fused kernel.  (Without the proxy fence
+    before a stage is released, a warp's outstanding shared-memory loads could
+    read the refilled stage: one warp row in 10^5 went wrong, differently in
+    every run.)"""
+    w = synth.CONFIGS["weak"].scaled(nz=64, corrections=FD, precision=prec)
+    rho, u = synth.random_fields(w.nx, w.ny, w.nz, 2024)
+    hs = [_lattice(P, monkeypatch, w, {}, t, graphs=1) for t in (False, True, True)]
+    for g in hs:
+        g.init_fields(rho, u)
+        g.step(12)
+    fa, fb, fc = (g.get_populations() for g in hs)
+    for g in hs:
+        g.close()
+    assert np.array_equal(fb, fc)
+    assert np.array_equal(fa, fb)
