@@ -307,3 +307,64 @@ def test_random_fd_problem_tma_kernel_matches_oracle(P, i, monkeypatch):
         pytest.skip("unstable draw: the oracle's state blows up (S:L407 criterion or 4x growth)")
     spread = _fp32_spread(kw, f0, steps) if kw["precision"] == 1 else 0.0
     _assert_close(fg, fo, kw["precision"], (kw, gpu), spread)
+
+
+N_SHAPE_CASES = int(os.environ.get("LBM_FUZZ_SHAPE_CASES", "12"))
+
+
+def _shape_cases():
+    """Random paper-rate problem statements (omega_1 = omega_high = 1, the
+    central-moment model: the collision of the plane-shape kernels) on the
+    compiled-in 256 x 256 plane, 3 planes: random walls / lid / free slip /
+    periodic faces, aspect ratios, cs2, omega_nu, omega_xi, force, correction
+    mode (FULL_FD through its two-pass path there: the TMA kernel needs z
+    periodic or ghost faces), precision, and two-buffer or AA streaming
+    (k_aa_shape)."""
+    rng = np.random.Generator(np.random.PCG64(2561))
+    out = []
+    while len(out) < N_SHAPE_CASES:
+        kw, _ = _draw(rng)
+        kw.update(nx=256, ny=256, nz=3, omega_1=1.0, omega_high=1.0, model=0)
+        gpu = dict(graphs=int(rng.integers(0, 3)))
+        fd = kw["corrections"] in (synth.CORR_FULL_FD, synth.CORR_FULL_FD_LAG)
+        if not fd and rng.random() < 0.5:
+            gpu["streaming"] = 1
+        out.append((kw, gpu))
+    return out
+
+
+SHAPE_CASES = _shape_cases()
+
+
+@pytest.mark.parametrize("i", range(N_SHAPE_CASES))
+def test_random_problem_shape_kernels_match_oracle(P, i):
+    """The plane-shape kernels (k_collide_stream_paper_shape / k_aa_shape, the
+    default at the BASELINE planes) on random problem statements against the
+    oracle, element by element after 13 steps (bars as above)."""
+    import oracle as O
+
+    kw, gpu = SHAPE_CASES[i]
+    try:
+        g = P.Lattice(**kw, **gpu)
+    except P.LbmError as e:
+        assert e.code in (P.lbm.LBM_EINVAL, P.lbm.LBM_ENOTSUP), e
+        pytest.skip(f"rejected by the ABI: {e}")
+    assert "_shape<" in g.kernel_name() or "fd_tma" in g.kernel_name(), g.kernel_name()
+    o = O.Oracle(**kw)
+    nx, ny, nz = kw["nx"], kw["ny"], kw["nz"]
+    rho, u = synth.random_fields(nx, ny, nz, 800 + i)
+    o.init_fields(rho, u)
+    f0 = o.get_populations() * (1.0 + 1e-3 * synth.noise((27, nz, ny, nx), 1800 + i))
+    o.set_populations(f0)
+    g.set_populations(f0)
+    steps = 13
+    o.step(steps)
+    g.step(steps)
+    g.sync()
+    fo, fg = o.get_populations(), g.get_populations()
+    g.close()
+    assert np.all(np.isfinite(fg)) or not _stable(o, f0)
+    if not _stable(o, f0):
+        pytest.skip("unstable draw: the oracle's state blows up (S:L407 criterion or 4x growth)")
+    spread = _fp32_spread(kw, f0, steps) if kw["precision"] == 1 else 0.0
+    _assert_close(fg, fo, kw["precision"], (kw, gpu), spread)
