@@ -14,8 +14,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
 VARIANTS = {
-    "walls_branch": [],
-    "walls_nobranch": ["LBM_FD_TMA_GRADBRANCH=0"],
+    "xfast": [],
+    "yfast": ["LBM_FD_YFAST=1"],
 }
 
 if sys.argv[1] == "build":
