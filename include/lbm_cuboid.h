@@ -269,7 +269,8 @@ int lbm_cuboid_info(const lbm_cuboid_t *h, int64_t out[8]);
 void *lbm_cuboid_stream(const lbm_cuboid_t *h);
 
 /* Name of the collide-stream kernel this handle's steps launch (e.g.
- * "k_collide_stream_paper_shape<double,512,512>"; "+ k_density" for the
+ * "k_collide_stream_paper_shape<double,512,512>"; "k_collide_stream_fd_tma<double>"
+ * for FULL_FD through the TMA-staged fused kernel; "+ k_density" for the
  * two-pass FULL_FD), for profiles and the bench's roofline record.  Valid until
  * the next call on the handle; "" for NULL. */
 const char *lbm_cuboid_kernel_name(const lbm_cuboid_t *h);

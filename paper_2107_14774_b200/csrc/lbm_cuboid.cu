@@ -1325,6 +1325,8 @@ int lbm_cuboid_create(const lbm_cuboid_params* p, lbm_cuboid_t** out) {
     const bool fdt_ok = h->fd && !h->fd_lag && !h->aa && zok(h->c.face[4]) && zok(h->c.face[5]) &&
                         (size_t(p->nx) * h->elem) % 16 == 0 && (align % 16) == 0;
     bool fdt_on = fdt_ok && fd_tma_staged_fraction(p->nx, p->ny, h->c.face[0] == lbm::FK_WRAP) >= 0.75;
+    // an explicit LBM_FD_FUSED selects the LDG fused / two-pass path unless LBM_FD_TMA=1 too
+    if (std::getenv("LBM_FD_FUSED")) fdt_on = false;
     if (const char* e = std::getenv("LBM_FD_TMA")) fdt_on = fdt_ok && std::atoi(e) != 0;
     h->fd_tma = fdt_on;
     if (h->fd_tma) {
