@@ -13,9 +13,15 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
+# The EARLY / MAXNREG switches below belonged to an experiment whose kernel code
+# was removed after measuring it slower (profiles/r2/fd_tma_variants.jsonl);
+# with the current sources they are no-ops.
 VARIANTS = {
-    "xfast": [],
-    "yfast": ["LBM_FD_YFAST=1"],
+    "base": ["LBM_FD_TMA_EARLY=0"],
+    "early": ["LBM_FD_TMA_EARLY=1"],
+    "early_m32_2": ["LBM_FD_TMA_EARLY=1", "LBM_FD_TMA_MINB32=2"],
+    "early_r200": ["LBM_FD_TMA_EARLY=1", "LBM_FD_TMA_MAXNREG=1"],
+    "base_r200": ["LBM_FD_TMA_EARLY=0", "LBM_FD_TMA_MAXNREG=1"],
 }
 
 if sys.argv[1] == "build":
