@@ -23,6 +23,7 @@ from __future__ import annotations
 import argparse
 import glob
 import hashlib
+import stat
 import json
 import os
 import subprocess
@@ -281,6 +282,19 @@ def run_cuda(args):
             raise SystemExit("--gpus N > 1 must be launched with torchrun --nproc-per-node N")
     torch.cuda.set_device(local)
     if world > 1:
+        # NCCL's own INIT lines (rank / nranks of every communicator) for the record: NCCL
+        # reads these once, at its first call, which is the torch process group's eager
+        # init below.  They go to stderr when that is a pipe or terminal (so rank 0's
+        # stdout stays the one JSON line; NCCL would truncate a regular file it reopens),
+        # else to stdout, NCCL's default
+        if "NCCL_DEBUG" not in os.environ:
+            os.environ["NCCL_DEBUG"] = "INFO"
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            try:
+                if not stat.S_ISREG(os.fstat(2).st_mode):
+                    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+            except OSError:
+                pass
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     w = workload(args, world)
     z0, z1 = synth.slab_range(w.nz, rank, world)
@@ -290,9 +304,6 @@ def run_cuda(args):
     if args.halo == "p2p":
         kw["halo"] = P.HALO_P2P
     if world > 1:
-        # NCCL's own INIT lines (rank / nranks of every communicator) for the record
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
-        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         lat = P.distributed_lattice(device=local, **kw)
     elif args.halo == "nccl":
         lat = P.Lattice(device=local, halo=P.HALO_NCCL, nccl_uid=P.nccl_unique_id(), **kw)
