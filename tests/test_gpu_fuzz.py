@@ -29,6 +29,9 @@ pytestmark = pytest.mark.gpu
 import os
 
 N_CASES = int(os.environ.get("LBM_FUZZ_CASES", "200"))  # more for a one-off stress run
+# a stress run on fresh draws: every generator seed below (problem statements and
+# fields) is shifted by this (0, the default, is the committed suite)
+SEED_OFFSET = int(os.environ.get("LBM_FUZZ_SEED_OFFSET", "0"))
 PER, BB, MW, FS = 0, 1, 2, 3
 
 
@@ -135,7 +138,7 @@ def _draw(rng):
 
 
 def _cases():
-    rng = np.random.Generator(np.random.PCG64(2107))
+    rng = np.random.Generator(np.random.PCG64(2107 + 7919 * SEED_OFFSET))
     return [_draw(rng) for _ in range(N_CASES)]
 
 
@@ -156,7 +159,7 @@ def test_random_problem_matches_oracle(P, i):
         pytest.skip(f"rejected by the ABI: {e}")
     o = O.Oracle(**kw)
     nx, ny, nz = kw["nx"], kw["ny"], kw["nz"]
-    rho, u = synth.random_fields(nx, ny, nz, 500 + i)
+    rho, u = synth.random_fields(nx, ny, nz, 500 + i + 100003 * SEED_OFFSET)
     o.init_fields(rho, u)
     f0 = o.get_populations() * (1.0 + 1e-3 * synth.noise((27, nz, ny, nx), 900 + i))
     o.set_populations(f0)
@@ -181,7 +184,7 @@ N_SLAB_CASES = int(os.environ.get("LBM_FUZZ_SLAB_CASES", "40"))
 
 
 def _slab_cases():
-    rng = np.random.Generator(np.random.PCG64(7413))
+    rng = np.random.Generator(np.random.PCG64(7413 + 7919 * SEED_OFFSET))
     out = []
     while len(out) < N_SLAB_CASES:
         kw, _ = _draw(rng)
@@ -215,7 +218,7 @@ def test_random_problem_p2p_slabs_match_oracle(P, i):
         h.p2p_connect(*P.lbm.p2p_neighbour_blobs(P.lbm.halo_plan(h.p), blobs))
     o = O.Oracle(**kw)
     nx, ny, nz = kw["nx"], kw["ny"], kw["nz"]
-    rho, u = synth.random_fields(nx, ny, nz, 700 + i)
+    rho, u = synth.random_fields(nx, ny, nz, 700 + i + 100003 * SEED_OFFSET)
     o.init_fields(rho, u)
     f0 = o.get_populations() * (1.0 + 1e-3 * synth.noise((27, nz, ny, nx), 1700 + i))
     o.set_populations(f0)
@@ -249,7 +252,7 @@ def _fdtma_cases():
     kernel stages most tiles (nx a multiple of 32 >= 64 or wider with x walls,
     ny >= 12), z periodic (its domain), any x / y boundary kinds, either model,
     rates, force, precision, launch and halo mode."""
-    rng = np.random.Generator(np.random.PCG64(1474))
+    rng = np.random.Generator(np.random.PCG64(1474 + 7919 * SEED_OFFSET))
     out = []
     while len(out) < N_FDTMA_CASES:
         kw, gpu = _draw(rng)
@@ -291,7 +294,7 @@ def test_random_fd_problem_tma_kernel_matches_oracle(P, i, monkeypatch):
     assert "fd_tma" in g.kernel_name(), g.kernel_name()
     o = O.Oracle(**kw)
     nx, ny, nz = kw["nx"], kw["ny"], kw["nz"]
-    rho, u = synth.random_fields(nx, ny, nz, 300 + i)
+    rho, u = synth.random_fields(nx, ny, nz, 300 + i + 100003 * SEED_OFFSET)
     o.init_fields(rho, u)
     f0 = o.get_populations() * (1.0 + 1e-3 * synth.noise((27, nz, ny, nx), 1300 + i))
     o.set_populations(f0)
@@ -320,7 +323,7 @@ def _shape_cases():
     mode (FULL_FD through its two-pass path there: the TMA kernel needs z
     periodic or ghost faces), precision, and two-buffer or AA streaming
     (k_aa_shape)."""
-    rng = np.random.Generator(np.random.PCG64(2561))
+    rng = np.random.Generator(np.random.PCG64(2561 + 7919 * SEED_OFFSET))
     out = []
     while len(out) < N_SHAPE_CASES:
         kw, _ = _draw(rng)
@@ -352,7 +355,7 @@ def test_random_problem_shape_kernels_match_oracle(P, i):
     assert "_shape<" in g.kernel_name() or "fd_tma" in g.kernel_name(), g.kernel_name()
     o = O.Oracle(**kw)
     nx, ny, nz = kw["nx"], kw["ny"], kw["nz"]
-    rho, u = synth.random_fields(nx, ny, nz, 800 + i)
+    rho, u = synth.random_fields(nx, ny, nz, 800 + i + 100003 * SEED_OFFSET)
     o.init_fields(rho, u)
     f0 = o.get_populations() * (1.0 + 1e-3 * synth.noise((27, nz, ny, nx), 1800 + i))
     o.set_populations(f0)
