@@ -299,6 +299,17 @@ def run_cuda(args):
     w = workload(args, world)
     z0, z1 = synth.slab_range(w.nz, rank, world)
     kw = w.params()
+    aa_fit_note = None
+    if args.streaming == "ab":
+        # two population buffers that do not fit in this GPU's free HBM (config 5 strong,
+        # 1024 x 1024 x 512, on one GPU: 2 x 116 GB): the one-buffer AA scheme instead, said so
+        from paper_2107_14774_b200 import lbm as _L
+        need = 2 * _L.buffer_bytes(_L.make_params(**dict(kw, rank=rank, world=world, device=local)))
+        free = torch.cuda.mem_get_info(local)[0]
+        if need > 0.95 * free:
+            args.streaming = "aa"
+            aa_fit_note = (f"AA in place (1 buffer): two buffers ({need / 2**30:.1f} GiB) exceed the "
+                           f"free HBM ({free / 2**30:.1f} GiB)")
     if args.streaming == "aa":
         kw["streaming"] = P.STREAM_AA
     if args.halo == "p2p":
@@ -458,7 +469,7 @@ def run_cuda(args):
                        "parallelism": f"z-slab x{world}" if world > 1 else "single GPU",
                        "nccl_comm": dict(zip(("nranks", "rank"), lat.comm_ranks())),
                        "halo": {0: "in-kernel wrap", 1: "nccl ghost planes", 2: "fused p2p ghost planes"}[lat.info()["halo"]],
-                       "streaming": "AA in place (1 buffer)" if args.streaming == "aa" else "AB (2 buffers)"},
+                       "streaming": aa_fit_note or ("AA in place (1 buffer)" if args.streaming == "aa" else "AB (2 buffers)")},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "bad_nodes": bad}
     print(json.dumps(line), flush=True)

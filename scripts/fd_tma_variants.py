@@ -18,6 +18,7 @@ VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
 # with the current sources they are no-ops.
 VARIANTS = {
     "base": ["LBM_FD_TMA_EARLY=0"],
+    "shape": ["LBM_FD_TMA_SHAPE=1"],
     "early": ["LBM_FD_TMA_EARLY=1"],
     "early_m32_2": ["LBM_FD_TMA_EARLY=1", "LBM_FD_TMA_MINB32=2"],
     "early_r200": ["LBM_FD_TMA_EARLY=1", "LBM_FD_TMA_MAXNREG=1"],
