@@ -13,8 +13,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
-# The EARLY / MAXNREG switches below belonged to an experiment whose kernel code
-# was removed after measuring it slower (profiles/r2/fd_tma_variants.jsonl);
+# The EARLY / MAXNREG / SHAPE switches below belonged to experiments whose kernel code
+# was removed after measuring them slower (profiles/r2/fd_tma_variants.jsonl);
 # with the current sources they are no-ops.
 VARIANTS = {
     "base": ["LBM_FD_TMA_EARLY=0"],
