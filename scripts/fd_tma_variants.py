@@ -13,13 +13,16 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VDIR = os.path.join(ROOT, "varbuild")  # git-ignored, travels to the GPU box
-# The EARLY / MAXNREG / SHAPE / RING3 switches below belonged to experiments whose kernel code
+# The EARLY / MAXNREG / SHAPE / RING3 / PF switches below belonged to experiments whose kernel code
 # was removed after measuring them slower (profiles/r2/fd_tma_variants.jsonl);
 # with the current sources they are no-ops.
 VARIANTS = {
     "base": ["LBM_FD_TMA_EARLY=0"],
     "shape": ["LBM_FD_TMA_SHAPE=1"],
     "ring3": ["LBM_FD_TMA_RING3=1"],
+    "pf1": ["LBM_FD_TMA_PF=1"],
+    "pf2": ["LBM_FD_TMA_PF=2"],
+    "pf4": ["LBM_FD_TMA_PF=4"],
     "early": ["LBM_FD_TMA_EARLY=1"],
     "early_m32_2": ["LBM_FD_TMA_EARLY=1", "LBM_FD_TMA_MINB32=2"],
     "early_r200": ["LBM_FD_TMA_EARLY=1", "LBM_FD_TMA_MAXNREG=1"],
