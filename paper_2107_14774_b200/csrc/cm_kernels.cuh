@@ -643,8 +643,14 @@ struct StorePushInterior {  // AA odd step, interior node: f~_q(x) -> slot q of 
   }
 };
 
+// fp32 storage: 7 resident 128-thread CTAs per SM (the odd kernel 96 -> 72
+// registers): 27.1 k vs 25.9 k MLUPS at 512^3 (profiles/r2/aa_minb.jsonl); with
+// fp64 the same bound measured 1.4 % slower, so it keeps LBM_MINB
+#ifndef LBM_AA_MINB32
+#define LBM_AA_MINB32 7
+#endif
 template <typename T, bool ODD, int SNX, int SNY>
-__global__ void LBM_CS_BOUNDS k_aa_shape(T* buf, const __grid_constant__ Consts c0, int zbeg, int zstride) {
+__global__ void __launch_bounds__(kBlock, sizeof(T) == 4 ? LBM_AA_MINB32 : LBM_MINB) k_aa_shape(T* buf, const __grid_constant__ Consts c0, int zbeg, int zstride) {
   Consts c = c0;
   c.nx = SNX;
   c.ny = SNY;
