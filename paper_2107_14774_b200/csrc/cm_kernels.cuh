@@ -178,8 +178,15 @@ __global__ void LBM_CS_BOUNDS_FD(FD) k_collide_stream_paper(const T* __restrict_
 // 26-neighbour density stencil gets immediate offsets too).  Instantiated for the
 // plane shapes of the BASELINE configs 3-5 (lbm_cuboid.cu, launch_cs); other
 // shapes use the general kernel.
+// fp32 storage: 7 resident 128-thread CTAs per SM (78 -> 72 registers): 28.9-29.0 k
+// vs 28.6 k MLUPS at 512^3, 30.1 k vs 29.1 k on the config-3 cavity, 27.5 k vs
+// 27.2 k over 600 steps (profiles/r2/shape_minb32.jsonl; 8 CTAs: slower)
+#ifndef LBM_SHAPE_MINB32
+#define LBM_SHAPE_MINB32 7
+#endif
 template <typename T, int SNX, int SNY, bool FD>
-__global__ void LBM_CS_BOUNDS_FD(FD) k_collide_stream_paper_shape(const T* __restrict__ src, T* __restrict__ dst,
+__global__ void __launch_bounds__(kBlock, (FD) ? LBM_FD_CS_MINB : ((sizeof(T) == 4 && LBM_SHAPE_MINB32) ? LBM_SHAPE_MINB32 : LBM_MINB))
+    k_collide_stream_paper_shape(const T* __restrict__ src, T* __restrict__ dst,
                                                                   const double* __restrict__ rf,
                                                                   const __grid_constant__ Consts c0, int zbeg,
                                                                   int zstride) {
